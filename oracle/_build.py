@@ -1,0 +1,26 @@
+"""Build the CPU oracle shared library (plain C, gcc).
+
+TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py.
+"""
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "fskmc_oracle.c")
+LIB = os.path.join(HERE, "_fskmc_oracle.so")
+
+
+def build(force: bool = False) -> str:
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= os.path.getmtime(SRC):
+        return LIB
+    # -ffp-contract=off: the clock arithmetic is the IEEE operation sequence of
+    # DESIGN.md §3 (no fused multiply-add contraction).
+    cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+           "-Wall", "-Wno-unused-function", "-o", LIB + ".tmp", SRC, "-lm"]
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True))

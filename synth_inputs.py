@@ -1,0 +1,60 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and bench.py.
+
+Holds none of the method's arithmetic: it only draws initial lattices and
+parameter sets ("input recipe").  Both the CUDA path (through
+kmc_set_config) and the oracle receive the same uint8 arrays from here.
+"""
+import numpy as np
+
+SEED_BASE = 0x5EED0001
+
+
+def bernoulli_lattice(shape, p=0.5, seed=SEED_BASE):
+    """Sites occupied (state 1) independently with probability p; uint8 site-major."""
+    rng = np.random.default_rng(seed)
+    return (rng.random(shape) < p).astype(np.uint8)
+
+
+def categorical_lattice(shape, probs, seed=SEED_BASE):
+    """Sites in state s with probability probs[s] (ZGB: 0 vacant, 1 CO, 2 O)."""
+    rng = np.random.default_rng(seed)
+    return rng.choice(len(probs), size=shape, p=probs).astype(np.uint8)
+
+
+def colour_full_lattice(shape, ndim, cell, C, colour=1):
+    """R#/P5 asymmetric start: sites of cells with the given colour full, others empty."""
+    R, H, W = shape
+    if ndim == 1:
+        qy, qx = 1, cell[0]
+    else:
+        qy, qx = cell
+    cy = np.arange(H)[:, None] // qy
+    cx = np.arange(W)[None, :] // qx
+    if C == 2:
+        col = (cx & 1) if ndim == 1 else ((cx + cy) & 1)
+    else:
+        col = (cx & 1) + 2 * (cy & 1)
+    col = np.broadcast_to(col, (H, W))
+    return np.broadcast_to((col == colour).astype(np.uint8), shape).copy()
+
+
+# Named workloads.
+WORKLOADS = {
+    # target / bench N=1: 2D Ising ads/des 32768^2, 8x8 cells, Lie dt=1,
+    # K=1, ca=cd=1, beta=1.5, h_dyn=-2 (paper's h=2 zero-field point), Bernoulli(1/2)
+    "ising2d_32768": dict(ndim=2, dims=(32768, 32768), cell=(8, 8), kind="adsdes",
+                          params=dict(ca=1.0, cd=1.0, beta=1.5, K=1.0, h=-2.0),
+                          scheme="lie", dt=1.0, init=0.5),
+    "ising2d_1024": dict(ndim=2, dims=(1024, 1024), cell=(8, 8), kind="adsdes",
+                         params=dict(ca=1.0, cd=1.0, beta=1.5, K=1.0, h=-2.0),
+                         scheme="lie", dt=1.0, init=0.5),
+    "ising1d_65536": dict(ndim=1, dims=(65536,), cell=(32,), kind="adsdes",
+                          params=dict(ca=1.0, cd=1.0, beta=2.0, K=1.0, h=0.0),
+                          scheme="lie", dt=1.0, init=0.0),
+    "diff2d_8192": dict(ndim=2, dims=(8192, 8192), cell=(8, 8), kind="adsdes_diff",
+                        params=dict(ca=1.0, cd=1.0, beta=1.5, K=1.0, h=-2.0, c_hop=1.0),
+                        scheme="strang", dt=1.0, init=0.5),
+    "zgb2d_32768": dict(ndim=2, dims=(32768, 32768), cell=(8, 8), kind="zgb",
+                        params=dict(k1=0.4, k2=1.0),
+                        scheme="lie", dt=0.1, init=0.0),
+}

@@ -1,0 +1,154 @@
+"""Pins of the brute-force master equation and the closed forms (CPU).
+
+The brute-force generator (oracle/bruteforce.py) is checked against what the
+paper and the mathematics fix: the non-interacting two-state law, the
+transfer matrix / eq.(exactcov1d), detailed balance (Gibbs invariance,
+P:981-985), generator additivity (eq.(gendecomp)), Lie/Strang local orders
+(eq.(error), eq.(error2)), the random-PCS mean error and the
+paper's printed closed-form values (tests/golden/paper_closed_forms.txt).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+from scipy.linalg import expm
+
+from oracle import bruteforce as bf
+from oracle import exact
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def ising(beta=1.0, K=1.0, h=-1.0, ca=1.0, cd=1.0):
+    return dict(kind="adsdes", ca=ca, cd=cd, beta=beta, K=K, h=h)
+
+
+def test_golden_paper_closed_forms():
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "paper_closed_forms.txt"))
+            if l.strip() and not l.startswith("#")]
+    for kind, b, h, val, tol in rows:
+        b, h, val, tol = float(b), float(h), float(val), float(tol)
+        if kind == "cov1d":
+            got = exact.paper_cov1d(b, 1.0, h)
+        elif kind == "cov2d":
+            got = exact.paper_cov2d(b, 1.0)
+        else:
+            got = exact.beta_c(1.0)
+        assert abs(got - val) <= tol, (kind, b, h, got, val)
+
+
+def test_generator_rows_sum_to_zero_and_additivity():
+    lat = bf.Lattice(1, 1, 6, 1, 2, 2)
+    Q, Qc, S = bf.generators(ising(), lat)
+    assert np.abs(np.asarray(Q.sum(axis=1))).max() < 1e-12
+    assert abs(Q - (Qc[0] + Qc[1])).max() < 1e-12          # eq.(gendecomp)
+    assert (Qc[0] - sp.diags(Qc[0].diagonal())).min() >= 0.0
+
+
+def test_noninteracting_closed_form_all_schemes():
+    """K = 0: [L^E, L^O] = 0 so every scheme is exact; per-site law is the
+    two-state closed form theta(t)."""
+    lat = bf.Lattice(1, 1, 6, 1, 1, 2)
+    m = ising(beta=1.0, K=0.0, h=0.3, ca=1.0, cd=0.5)
+    Q, Qc, S = bf.generators(m, lat)
+    p0 = bf.point_mass(S, lat.N, [0] * lat.N)
+    cov = bf.coverage_values(lat, S)
+    th = exact.noninteracting_theta(1.5, 1.0, 0.5, 1.0, 0.3)
+    for scheme in ("exact", "lie", "strang"):
+        p = bf.law(p0, Q, Qc, scheme, 0.5, 1.5, 2)
+        assert abs(p @ cov - th) < 1e-9, scheme
+    # random (SL) schedule: a site's colour is active in B ~ Binomial(C n, 1/C) of the
+    # C n windows, so its law is E_B[theta(B dt)] (eq.(SLPCS))
+    n, C, dt = 3, 2, 0.5
+    thr = sum(math.comb(C * n, b) * (1 / C) ** b * (1 - 1 / C) ** (C * n - b)
+              * exact.noninteracting_theta(b * dt, 1.0, 0.5, 1.0, 0.3) for b in range(C * n + 1))
+    p = bf.law(p0, Q, Qc, "random", dt, n * dt, C)
+    assert abs(p @ cov - thr) < 1e-9
+
+
+def test_gibbs_invariance_and_transfer_matrix():
+    """Detailed balance (R9): pi Q^c = 0 for every colour; the stationary
+    coverage equals the finite-N transfer matrix of the literal rates."""
+    N = 8
+    lat = bf.Lattice(1, 1, N, 1, 2, 2)
+    m = ising(beta=1.3, K=1.0, h=-0.4, ca=1.0, cd=0.7)
+    Q, Qc, S = bf.generators(m, lat)
+    A = Q.toarray()
+    w, v = np.linalg.eig(A.T)
+    pi = np.real(v[:, np.argmin(np.abs(w))])
+    pi = pi / pi.sum()
+    for Qk in Qc:
+        assert np.abs(pi @ Qk.toarray()).max() < 1e-12
+    cov = bf.coverage_values(lat, S)
+    tm = exact.tm_coverage_1d(N, 1.3, 1.0, -0.4, 1.0, 0.7)
+    assert abs(pi @ cov - tm) < 1e-12
+
+
+def test_transfer_matrix_vs_paper_formula_R9():
+    """Thermodynamic-limit TM of the literal rates equals eq.(exactcov1d) with the
+    R9 mapping h_paper = h_dyn + 2K."""
+    for beta in (1.0, 2.0, 4.0):
+        for hp in (0.0, 0.5, 1.0, 1.5, 2.0):
+            hd = exact.h_dyn_from_paper(hp, 1.0, 1)
+            assert abs(exact.tm_coverage_1d(None, beta, 1.0, hd) - exact.paper_cov1d(beta, 1.0, hp)) < 1e-12
+
+
+def _defect(Q, Qc, dt, scheme):
+    E = expm(dt * Q.toarray())
+    A, B = Qc[0].toarray(), Qc[1].toarray()
+    if scheme == "lie":
+        P = expm(dt * A) @ expm(dt * B)
+    else:
+        P = expm(0.5 * dt * A) @ expm(dt * B) @ expm(0.5 * dt * A)
+    return np.abs(E - P).max()
+
+
+def test_local_error_orders():
+    """eq.(error): Lie local error O(dt^2); eq.(error2): Strang O(dt^3)."""
+    lat = bf.Lattice(1, 1, 6, 1, 1, 2)
+    Q, Qc, S = bf.generators(ising(beta=1.0, K=1.0, h=-1.0, ca=0.2, cd=0.2), lat)
+    dt = 0.05
+    rl = _defect(Q, Qc, dt, "lie") / _defect(Q, Qc, dt / 2, "lie")
+    rs = _defect(Q, Qc, dt, "strang") / _defect(Q, Qc, dt / 2, "strang")
+    assert 3.6 < rl < 4.4
+    assert 7.2 < rs < 8.8
+
+
+def test_random_pcs_mean_error():
+    """E_xi[e^{dt A_xi1} e^{dt A_xi2}] - e^{dt(A1+A2)} = 1/4 (A1 - A2)^2 dt^2 + O(dt^3)."""
+    lat = bf.Lattice(1, 1, 4, 1, 1, 2)
+    Q, Qc, S = bf.generators(ising(beta=1.0, K=1.0, h=-1.0), lat)
+    A1, A2 = Qc[0].toarray(), Qc[1].toarray()
+    for dt in (1e-2, 5e-3):
+        avg = 0.25 * sum(expm(dt * X) @ expm(dt * Y) for X in (A1, A2) for Y in (A1, A2))
+        err = avg - expm(dt * (A1 + A2))
+        pred = 0.25 * (A1 - A2) @ (A1 - A2) * dt * dt
+        assert np.abs(err - pred).max() < 10 * dt ** 3 * np.abs(A1).max() ** 3
+
+
+def test_boundary_only_commutator():
+    """eq.(opdecomperror): [L^E, L^O] is supported on cell boundaries -- with
+    K = 0 (no interaction across cells) it vanishes."""
+    lat = bf.Lattice(1, 1, 6, 1, 2, 2)
+    Q, Qc, S = bf.generators(ising(K=0.0, h=0.2), lat)
+    A, B = Qc[0].toarray(), Qc[1].toarray()
+    assert np.abs(A @ B - B @ A).max() < 1e-12
+    Q, Qc, S = bf.generators(ising(K=1.0, h=-1.0), lat)
+    A, B = Qc[0].toarray(), Qc[1].toarray()
+    assert np.abs(A @ B - B @ A).max() > 1e-3
+
+
+def test_lie_order_asymmetric_start():
+    """Global weak error of Lie is O(dt) with an asymmetric start (R#-P5), Strang O(dt^2)."""
+    lat = bf.Lattice(1, 1, 8, 1, 2, 2)
+    Q, Qc, S = bf.generators(ising(beta=1.0, K=1.0, h=-1.0), lat)
+    conf = [1 if lat.colour(i) == 1 else 0 for i in range(lat.N)]
+    p0 = bf.point_mass(S, lat.N, conf)
+    cov = bf.coverage_values(lat, S)
+    ex = bf.law(p0, Q, Qc, "exact", 0, 2.0, 2) @ cov
+    el = [abs(bf.law(p0, Q, Qc, "lie", dt, 2.0, 2) @ cov - ex) for dt in (0.25, 0.125)]
+    es = [abs(bf.law(p0, Q, Qc, "strang", dt, 2.0, 2) @ cov - ex) for dt in (0.25, 0.125)]
+    assert 1.6 < el[0] / el[1] < 2.5
+    assert 3.2 < es[0] / es[1] < 5.0
