@@ -1,0 +1,303 @@
+"""Benchmark of the fractional-step KMC hot path (BASELINE.json metric: KMC events/s).
+
+python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload NAME]
+
+A step = one Lie macro-step (every colour's window: a2-a7) + the observables (a8) of the
+named workload (default: BASELINE's target, 2D Ising ads/des 32768^2, 8x8 cells, dt = 1),
+inputs resident in HBM.  N > 1: one process per GPU (torchrun), 2D slab decomposition with
+NCCL halo exchange, weak scaling (32768 x 32768 sites per GPU), max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth_inputs as si  # noqa: E402
+
+METRIC = "KMC events/sec (and site-updates/sec) at 1/2/4/8 B200; % of HBM peak"
+UNIT = "events/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline_sample(wl, seconds_hint="~10-30 s"):
+    """The O2 oracle as it stands, on a bounded sample of the workload (rank 0, N = 1)."""
+    from oracle.fskmc import FSKMC, model_params
+    side = 512
+    o = FSKMC(wl["ndim"], (side, side), wl["cell"], wl["kind"], model_params(**wl["params"]), seed=7)
+    o.set_config(si.bernoulli_lattice((1, side, side), wl["init"], seed=si.SEED_BASE + 1))
+    t0 = time.perf_counter()
+    nmacro = 2
+    o.run(nmacro * wl["dt"], wl["dt"], wl["scheme"])
+    el = time.perf_counter() - t0
+    return {"value": o.events / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"O2 oracle, {side}x{side} periodic sub-lattice of the workload, {nmacro} {wl['scheme']} "
+                      f"macro-steps dt={wl['dt']}, {o.events} events in {el:.1f} s, 1 thread"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (O2), timed on this host, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.fskmc import FSKMC, model_params
+    wl = si.WORKLOADS[args.workload]
+    side = 256
+    o = FSKMC(wl["ndim"], (side, side), wl["cell"], wl["kind"], model_params(**wl["params"]), seed=7)
+    o.set_config(si.bernoulli_lattice((1, side, side), wl["init"], seed=si.SEED_BASE + 1))
+    for _ in range(args.warmup):
+        o.run(wl["dt"], wl["dt"], wl["scheme"])
+    e0 = o.events
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.run(wl["dt"], wl["dt"], wl["scheme"])
+        o.observables()
+    el = time.perf_counter() - t0
+    v = (o.events - e0) / el
+    sample = f"O2 oracle on a {side}x{side} periodic sub-lattice of {args.workload}, 1 macro-step per step, 1 thread"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
+        "data": "synthetic", "config": {"workload": args.workload + f" (sample {side}x{side})"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kmc", choices=["kmc", "reference"])
+    ap.add_argument("--workload", default="ising2d_32768", choices=sorted(si.WORKLOADS))
+    ap.add_argument("--dt", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1105_4673_b200 as kmc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        box = [kmc.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
+
+    wl = dict(si.WORKLOADS[args.workload])
+    dt = args.dt if args.dt is not None else wl["dt"]
+    ndim = wl["ndim"]
+    if ndim == 2:
+        H1, W = wl["dims"]
+        gdims = (H1 * world, W)          # weak scaling: one H1 x W slab per GPU
+    else:
+        gdims = wl["dims"]
+    stream = torch.cuda.current_stream()
+    k = kmc.KMC(ndim, gdims, wl["cell"], kind=wl["kind"], replicas=wl.get("replicas", world if ndim == 1 else 1),
+                seed=0xB200, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=uid,
+                **wl["params"])
+    shape = k.local_shape
+    if wl["kind"].startswith("zgb"):
+        lat = si.categorical_lattice(shape, [1.0 - wl["init"], wl["init"] / 2, wl["init"] / 2] if wl["init"] else [1.0, 0.0, 0.0],
+                                     seed=si.SEED_BASE + rank)
+    else:
+        lat = si.bernoulli_lattice(shape, wl["init"], seed=si.SEED_BASE + rank)
+    host = torch.from_numpy(lat).pin_memory()
+    dev = host.to(f"cuda:{local}")
+    del lat
+    k.set_config_device(dev.data_ptr(), dev.numel())
+    sites = int(np.prod(gdims)) * (wl.get("replicas", 1))
+    C = 2 if (ndim == 1 or wl["kind"] == "adsdes") else 4
+
+    def step():
+        k.run(dt, dt, wl["scheme"])
+        return k.observables()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    obs0 = k.observables()
+    k.enable_timing(True)
+    k.timing(reset=True)
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        obs = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    kern_ms, launches = k.timing(reset=True)
+    k.enable_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    events = obs["events"] - obs0["events"]          # all ranks (NCCL all-reduce inside kmc_observables)
+    value = events / (ms / 1e3)
+    site_updates = sites * args.steps / (ms / 1e3)
+
+    # ---- e2e: through the public API with HOST buffers, H2D + D2H inside the timed region ----
+    host_np = host.numpy()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev_e2e = 0
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        k.set_config(host_np)                           # H2D of the step's input lattice (pinned)
+        o_a = k.observables()
+        k.run(dt, dt, wl["scheme"])
+        o_b = k.observables()                           # D2H of the step's result (counters)
+        ev_e2e += o_b["events"] - o_a["events"]
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (substep_kernel) ----
+    peaks, peak_src = load_peaks()
+    avg_launch_ms = kern_ms / max(1, launches)
+    events_per_launch = events / max(1, launches) / max(1, world)      # this rank's share
+    cells_per_launch = int(np.prod(shape)) / (64 if ndim == 2 else wl["cell"][0]) / C
+    # algorithmic HBM bytes per launch: per active cell read own + 4 neighbour words
+    # and write own word (8 B each) per plane, read-modify-write 4 B of the workload counter
+    nplanes = 2 if wl["kind"].startswith("zgb") else 1
+    nb = 2 * ndim
+    bytes_per_launch = cells_per_launch * (nplanes * 8 * (nb + 2) + 8)
+    hbm_gbs = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    prof = {}
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "substep_profile.json")))
+    except Exception:
+        pass
+    ipe = prof.get(wl["kind"], {}).get("warp_inst_per_event")
+    sm_clk = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    issue_peak = 148 * 4 * sm_clk * 1e6 / 1e9                              # G warp-inst / s
+    achieved = ipe * events_per_launch / (avg_launch_ms / 1e3) / 1e9 if ipe else None
+    roof = {"bound": "alu", "unit": "Gwarp-inst/s", "achieved": achieved, "peak": issue_peak,
+            "frac": (achieved / issue_peak) if achieved else None,
+            "peak_source": f"148 SMs x 4 schedulers x 1 warp-inst/clk x {sm_clk:.0f} MHz (median SM clock under load)",
+            "per_unit": f"{ipe} warp-inst/event (ncu sm__inst_executed / events, profiles/substep_profile.json)",
+            "traffic": prof.get(wl["kind"], {}).get("dram_bytes_per_launch"),
+            "kernel": "substep_kernel", "avg_launch_ms": avg_launch_ms, "launches": launches,
+            "kernel_share_of_step": kern_ms / ms,
+            "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
+                    "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch}}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(wl)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "dims_per_gpu": list(wl["dims"]), "cell": list(wl["cell"]),
+                   "model": wl["kind"], "params": wl["params"], "scheme": wl["scheme"], "dt": dt,
+                   "init": f"Bernoulli({wl['init']})", "colours": C,
+                   "l2": "inputs larger than L2 (bit-packed lattice 128 MiB/GPU at 32768^2 > 126 MB L2)",
+                   "parallelism": f"slab{world}" if ndim == 2 else f"replicas{world}"},
+        "site_updates_per_s": site_updates,
+        "events_per_step": events / args.steps,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": ev_e2e / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(host.numel()), "d2h_bytes_per_step": 2 * (37 * 8)},
+        "gpu_launches": int(launches + args.steps),
+        "clocks": clocks,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

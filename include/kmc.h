@@ -1,0 +1,171 @@
+/*
+ * kmc.h -- C ABI of the B200-native fractional-step kinetic Monte Carlo library
+ * (libkmc_b200.so, built from paper_1105_4673_b200/csrc/).
+ *
+ * Method: Arampatzis, Katsoulakis, Plechac, Taufer, Xu, "Hierarchical
+ * fractional-step approximations and parallel kinetic Monte Carlo algorithms"
+ * (arXiv:1105.4673).  "P:n" = line n of the paper text; "R#" = the
+ * readings listed in DESIGN.md §4; the arithmetic spec every result is
+ * bit-exact to is DESIGN.md §3.
+ *
+ * The lattice generator L (eq.(generator)) is split over coarse
+ * cells C_m (eq.(decomposition)) grouped into C colours
+ * (eq.(sublatt); C = 4 for cross-cell-writing models, R6) and
+ * advanced by a Lie (eq.(lie)), Strang (eq.(strang)) or
+ * random sub-lattice (eq.(SLPCS)/eq.(SL)) product.  Inside one
+ * window every cell of the active colour runs its own serial SSA
+ * (eq.(exact); eq.(totalrate); eq.(skeleton)).
+ *
+ * Conventions (all entry points):
+ *   - every call returns a kmc_status and never throws across the ABI; the
+ *     last error text is kept per context (kmc_last_error) or, for a failed
+ *     kmc_create, globally (kmc_create_error);
+ *   - the context owns every device buffer it allocates; pointers passed in
+ *     are borrowed for the duration of the call only;
+ *   - host lattice buffers are uint8, site-major [replica][y][x] over the
+ *     caller's LOCAL slab (rank-local rows in 2D, rank-local replicas in 1D);
+ *     spin values: adsdes 0 vacant / 1 occupied; zgb 0 vacant / 1 CO / 2 O;
+ *   - kmc_run / kmc_substep / kmc_*_device are stream-ordered and
+ *     asynchronous on the context's stream; kmc_observables, kmc_set_config
+ *     and kmc_get_config synchronise it.
+ */
+#ifndef KMC_B200_H
+#define KMC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kmc_ctx kmc_ctx;   /* opaque; owned by the library */
+
+typedef enum {
+    KMC_OK = 0,
+    KMC_EINVAL = 1,       /* bad argument (NULL, unknown enum, spin value out of range, size mismatch) */
+    KMC_EPARTITION = 2,   /* geometry violates R6/R7 (see kmc_create) */
+    KMC_ENOMEM = 3,       /* device or host allocation failed */
+    KMC_ECUDA = 4,        /* a CUDA runtime call or kernel failed (text in kmc_last_error) */
+    KMC_ENCCL = 5,        /* an NCCL call failed or libnccl could not be loaded */
+    KMC_ESTATE = 6,       /* call not valid in the context's current state */
+    KMC_WTRUNCATED = 100  /* warning, kmc_run: T not a multiple of dt, last macro-step shortened (R20) */
+} kmc_status;
+
+typedef enum { KMC_LIE = 0, KMC_STRANG = 1, KMC_RANDOM = 2 } kmc_scheme;
+
+/* Rate mechanisms.  Slot classes, canonical order:
+ *  ADSDES       eq.(Arrhenius) P:963-968 (literal rates, R9):
+ *               [adsorb c_a] [desorb c_d exp(-beta(K n + h)), n = 0..z]
+ *  ADSDES_DIFF  + Kawasaki hops x->x+e_d, y vacant, c_hop exp(-beta K n(x)) (R12),
+ *               d in (-x,+x,-y,+y), n = 0..z-1
+ *  ZGB          Table COrates P:1132-1148 (R13): [CO adsorb k1] [O2 adsorb (1-k1)/z per
+ *               vacant neighbour d] [CO+O react k2/z, CO anchor, d] [CO+O react k2/z, O anchor, d]
+ *  ZGB_DIFF     + CO hops c_hop per vacant neighbour d
+ *  z = 2 ndim.  */
+typedef enum { KMC_ADSDES = 0, KMC_ADSDES_DIFF = 1, KMC_ZGB = 2, KMC_ZGB_DIFF = 3 } kmc_model_kind;
+
+typedef struct {
+    int32_t kind;                 /* kmc_model_kind */
+    double ca, cd, beta, K, h;    /* Arrhenius ads/des (c1 = ca, c2 = cd) */
+    double c_hop;                 /* hop prefactor (R12; ZGB_DIFF: CO hop rate) */
+    double k1, k2;                /* ZGB (R14) */
+} kmc_model;
+
+typedef struct {
+    int32_t ndim;                 /* 1 or 2 */
+    int64_t dims[2];              /* 1D: dims[0] = N sites.  2D: dims[0] = H rows (y), dims[1] = W cols (x) */
+    int32_t cell[2];              /* 1D: cell[0] = Q.  2D: cell[0] = q_y, cell[1] = q_x;  q_x*q_y <= 64 */
+    int32_t colours;              /* 0 = auto (2 for spin-flip or 1D, 4 otherwise), else 2 or 4 */
+    int32_t replicas;             /* independent lattices batched (R21); global cell id = rep*M + m */
+    uint64_t seed;                /* Philox key (R17) */
+} kmc_geometry;
+
+typedef struct {
+    int32_t rank, world;          /* world = 1: single GPU.  world > 1: 2D slabs along y, 1D replicas split */
+    int32_t device;               /* CUDA device ordinal */
+    const uint8_t* nccl_unique_id;/* 128 bytes from kmc_nccl_unique_id() on rank 0, broadcast; NULL if world = 1 */
+    void* stream;                 /* cudaStream_t to launch on (e.g. torch's current stream); NULL = library-owned */
+} kmc_dist;
+
+typedef struct {
+    double time;                  /* physical time reached (sum of macro-step durations) */
+    uint64_t windows;             /* global window (sub-step) counter, persists across kmc_run */
+    uint64_t events;              /* executed SSA events since create (all ranks) */
+    int64_t n_state[4];           /* sites per state (all ranks) */
+    int64_t nn_pairs[4][4];       /* nearest-neighbour bonds {x,y} by unordered state pair, symmetric */
+    int64_t n_state_by_colour[4][4]; /* [cell colour][state] */
+    double coverage[4];           /* n_state / sites */
+    double energy;                /* R24: -K nn_pairs[1][1] + h n_state[1] (paper H) */
+} kmc_obs;
+
+/* Create a context.  Validates the geometry (KMC_EPARTITION when: dims not divisible by the
+ * cell, cell > 64 sites, odd number of cells per axis, cell extent < 2 for a cross-cell-writing
+ * model (R7), 2 colours for a cross-cell-writing 2D model (R6), 2D rows per rank not a multiple of
+ * 2 q_y, 1D replicas not divisible by world), builds the FP64 rate table and its u64 quantisation
+ * (R18), allocates the bit-packed device lattice (all sites vacant, R22), and -- world > 1 --
+ * initialises NCCL from the unique id.  On failure *out = NULL and kmc_create_error() explains. */
+kmc_status kmc_create(const kmc_geometry* geom, const kmc_model* model, const kmc_dist* dist, kmc_ctx** out);
+void kmc_destroy(kmc_ctx* ctx);
+const char* kmc_last_error(const kmc_ctx* ctx);
+const char* kmc_create_error(void);
+
+/* Local slab sizes: bytes of the uint8 host/device lattice buffer this rank exchanges, and its
+ * shape [replicas_local][rows_local][W] plus the global offsets of its first replica and row. */
+kmc_status kmc_local_shape(const kmc_ctx* ctx, int64_t* replicas_local, int64_t* rows_local,
+                           int64_t* width, int64_t* replica_offset, int64_t* row_offset);
+
+/* Copy the local slab in (validating spin values < number of states, else KMC_EINVAL and the
+ * lattice is unchanged) or out.  nbytes must equal replicas_local*rows_local*W.  Synchronous. */
+kmc_status kmc_set_config(kmc_ctx* ctx, const uint8_t* host_local_slab, int64_t nbytes);
+kmc_status kmc_get_config(kmc_ctx* ctx, uint8_t* host_local_slab, int64_t nbytes);
+/* Same with a device buffer (e.g. a torch CUDA tensor), stream-ordered, no validation report
+ * (out-of-range spins are clamped to vacant and counted; see kmc_observables). */
+kmc_status kmc_set_config_device(kmc_ctx* ctx, const uint8_t* dev_local_slab, int64_t nbytes);
+kmc_status kmc_get_config_device(kmc_ctx* ctx, uint8_t* dev_local_slab, int64_t nbytes);
+
+/* Advance physical time by T with macro-steps of dt (R20: n = ceil(T/dt - 1e-9) macro-steps, the
+ * last of duration T - (n-1) dt; KMC_WTRUNCATED if it differs from dt).  Lie: colours 0..C-1 for
+ * dt each; Strang: palindrome with half steps for colour 0 (R2); random: C windows per macro-step,
+ * colour xi_w drawn from Philox by global window id (R4).  Asynchronous. */
+kmc_status kmc_run(kmc_ctx* ctx, double T, double dt, kmc_scheme scheme);
+
+/* One window: every cell of colour `colour` runs its SSA for `duration` (eq.(exact)); the window
+ * counter advances by one, physical time does not.  Asynchronous. */
+kmc_status kmc_substep(kmc_ctx* ctx, int32_t colour, double duration);
+
+/* Observables at the current state (a8).  per_cell_events (nullable, host) receives the
+ * cumulative executed events of each LOCAL cell, uint32, in order [replica][cy][cx] (D5, eq.(wload)
+ * the workload of a window is the difference of two snapshots).  Synchronous; world > 1
+ * sums the counters over ranks (NCCL all-reduce). */
+kmc_status kmc_observables(kmc_ctx* ctx, kmc_obs* out, uint32_t* per_cell_events);
+
+/* Checkpoint / resume: the whole state is (lattice, window counter, time, seed, config). */
+kmc_status kmc_get_state(const kmc_ctx* ctx, uint64_t* windows, double* time);
+kmc_status kmc_set_state(kmc_ctx* ctx, uint64_t windows, double time);
+
+/* Inspection of the rate table (a1): n classes with type/dir/kappa, FP64 rate, u64 fixed point
+ * and the scale exponent F (rate_u64 = llround(rate 2^F)).  Arrays hold >= 32 entries. */
+kmc_status kmc_rate_table(const kmc_ctx* ctx, int32_t* n, int32_t* type, int32_t* dir, int32_t* kappa,
+                          double* rate, uint64_t* rate_u64, int32_t* F);
+
+/* Kernel timing (bench): when enabled, every sub-step kernel is bracketed by CUDA events on the
+ * launching stream; kmc_timing returns the summed kernel milliseconds and launch count since the
+ * last reset (synchronises). */
+kmc_status kmc_enable_timing(kmc_ctx* ctx, int32_t enable);
+kmc_status kmc_timing(kmc_ctx* ctx, double* kernel_ms, int64_t* launches, int32_t reset);
+
+/* Host-side partition plan for rank `rank` of `world` (no device work): owned rows / replicas and
+ * ring neighbours.  out[0] = replica_offset, out[1] = replicas_local, out[2] = row_offset,
+ * out[3] = rows_local, out[4] = rank above (-y neighbour, -1 if none), out[5] = rank below. */
+kmc_status kmc_partition_plan(const kmc_geometry* geom, int32_t kind, int32_t world, int32_t rank, int64_t out[6]);
+
+/* NCCL unique id for world > 1 (rank 0 calls it and broadcasts the 128 bytes). */
+kmc_status kmc_nccl_unique_id(uint8_t out[128]);
+
+/* Library version string. */
+const char* kmc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMC_B200_H */

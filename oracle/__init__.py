@@ -53,6 +53,11 @@ def lib():
                                  ctypes.c_int, ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64,
                                  ctypes.c_int, ip, ip, ip, u64p, ctypes.c_int, ctypes.c_void_p]
         L.orc_window.restype = ctypes.c_int64
+        L.orc_window_cells.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                       ctypes.c_int64, ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64,
+                                       ctypes.c_int, ip, ip, ip, u64p, ctypes.c_int, ctypes.c_void_p]
+        L.orc_window_cells.restype = ctypes.c_int64
         L.orc_ssa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                               ctypes.c_int, ip, ip, ip, u64p, ctypes.c_int, ctypes.c_uint64,
                               ctypes.c_uint32, dp, ctypes.c_int, ctypes.c_void_p]

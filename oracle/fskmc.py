@@ -159,6 +159,22 @@ class FSKMC:
         self.events += int(ev)
         return int(ev)
 
+    def window_cells(self, cells, D: float, window: int):
+        """Run window `window` (duration D) on the listed cells only ([n][3] = replica, cy, cx,
+        all of one colour), in place; returns the per-cell event counts.  Used to check sampled
+        cells of a full-size GPU window from the pre-window lattice (cells are independent)."""
+        t = self.table
+        ip = ctypes.POINTER(ctypes.c_int)
+        cells = np.ascontiguousarray(cells, dtype=np.int64).reshape(-1, 3)
+        ev = np.zeros(len(cells), dtype=np.uint32)
+        lib().orc_window_cells(
+            self.lat.ctypes.data, self.R, self.H, self.W, self.ndim, self.qx, self.qy,
+            cells.ctypes.data, len(cells), float(D), int(window), self.seed,
+            t["n"], t["type"].ctypes.data_as(ip), t["dir"].ctypes.data_as(ip),
+            t["kappa"].ctypes.data_as(ip), t["rate_u64"].ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+            t["F"], ev.ctypes.data)
+        return ev
+
     def macro_step(self, scheme: int, d: float) -> int:
         ev = 0
         for colour, D in substeps(scheme, self.C, d, self.seed, self.window):

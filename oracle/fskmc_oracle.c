@@ -287,9 +287,74 @@ int orc_cell_colour(int ndim, int C, int64_t cy, int64_t cx)
 }
 
 /* ------------------------------------------------------------------ */
-/* O2: one window of colour `colour` and duration D on all replicas.   */
-/* Returns the number of executed events; W_events[gid] += events.     */
+/* O2: one window for ONE cell (r, cy, cx): the serial SSA of the cell for time D.  */
+/* Returns the number of executed events.                                          */
 /* ------------------------------------------------------------------ */
+static uint32_t cell_window(latview* L, int64_t rep, int64_t cy, int64_t cx, int qx, int qy,
+                            uint64_t gid, double D, uint64_t window, const uint32_t key[2],
+                            int nclass, const int* ctype, const int* cdir, const int* ckappa,
+                            const uint64_t* crate_u64, double inv_scale)
+{
+    const int nsite = qx * qy;
+    /* member[c][s] = 1 if slot class c is eligible at local site s */
+    uint8_t member[MAXCLASS][64];
+    double t = 0.0;
+    uint32_t k = 0;
+    for (;;) {
+        /* eq.(totalrate) restricted to the cell: enumerate slots in canonical order */
+        uint64_t cnt[MAXCLASS];
+        uint64_t lam = 0;
+        for (int c = 0; c < nclass; ++c) {
+            cnt[c] = 0;
+            for (int s = 0; s < nsite; ++s) {
+                int64_t y = cy * qy + s / qx, x = cx * qx + s % qx;
+                int kap;
+                int el = slot_kappa(L, rep, y, x, ctype[c], cdir[c], &kap) && kap == ckappa[c];
+                member[c][s] = (uint8_t)el;
+                cnt[c] += (uint64_t)el;
+            }
+            lam += cnt[c] * crate_u64[c];
+        }
+        if (lam == 0) break;                               /* quiescent cell */
+        uint32_t ctr[4] = {k, (uint32_t)gid, (uint32_t)window,
+                           (uint32_t)((window >> 32) & 0x0FFFFFFFu) | (0u << 28)};
+        uint32_t xr[4];
+        orc_philox4x32_10(ctr, key, xr);
+        /* exponential clock, eq.(totalrate): tau = -ln U / lambda */
+        uint64_t j53 = ((uint64_t)xr[0] << 21) | (uint64_t)(xr[1] >> 11);
+        double U = (double)(j53 + 1) * 0x1p-53;
+        double E = -orc_log(U);
+        double lamd = (double)lam * inv_scale;
+        double tau = E / lamd;
+        if (t + tau >= D) break;                           /* R5: pending event discarded */
+        t = t + tau;
+        /* eq.(skeleton): class with prob cnt*rate/lambda, then a uniform member site */
+        uint64_t r = (uint64_t)(((unsigned __int128)xr[2] * (unsigned __int128)lam) >> 32);
+        uint64_t cum = 0;
+        int csel = -1;
+        for (int c = 0; c < nclass; ++c) {
+            cum += cnt[c] * crate_u64[c];
+            if (cum > r) { csel = c; break; }
+        }
+        uint64_t kk = ((uint64_t)xr[3] * cnt[csel]) >> 32;
+        int ssel = -1;
+        uint64_t seen = 0;
+        for (int s = 0; s < nsite; ++s) {
+            if (member[csel][s]) {
+                if (seen == kk) { ssel = s; break; }
+                ++seen;
+            }
+        }
+        int64_t y = cy * qy + ssel / qx, x = cx * qx + ssel % qx;
+        apply_slot(L, rep, y, x, ctype[csel], cdir[csel]);
+        ++k;
+    }
+    return k;
+}
+
+/* O2: one window of colour `colour` and duration D on all replicas (eq.(exact): the cells of
+ * one colour are independent, so processing them in any order in place is exact).
+ * Returns the number of executed events; W_events[gid] += events. */
 int64_t orc_window(uint8_t* lat, int R, int64_t H, int64_t W, int ndim, int qx, int qy,
                    int C, int colour, double D, uint64_t window, uint64_t seed,
                    int nclass, const int* ctype, const int* cdir, const int* ckappa,
@@ -297,70 +362,41 @@ int64_t orc_window(uint8_t* lat, int R, int64_t H, int64_t W, int ndim, int qx, 
 {
     latview L = {lat, H, W, ndim};
     const int64_t Mx = W / qx, My = H / qy;
-    const int nsite = qx * qy;
     const double inv_scale = ldexp(1.0, -F);          /* 2^-F */
     const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     int64_t total = 0;
-    /* member[c][s] = 1 if slot class c is eligible at local site s */
-    uint8_t member[MAXCLASS][64];
-
     for (int64_t rep = 0; rep < R; ++rep)
     for (int64_t cy = 0; cy < My; ++cy)
     for (int64_t cx = 0; cx < Mx; ++cx) {
         if (orc_cell_colour(ndim, C, cy, cx) != colour) continue;
         const uint64_t gid = (uint64_t)rep * (uint64_t)(Mx * My) + (uint64_t)(cy * Mx + cx);
-        double t = 0.0;
-        uint32_t k = 0;
-        for (;;) {
-            /* eq.(totalrate) restricted to the cell: enumerate slots in canonical order */
-            uint64_t cnt[MAXCLASS];
-            uint64_t lam = 0;
-            for (int c = 0; c < nclass; ++c) {
-                cnt[c] = 0;
-                for (int s = 0; s < nsite; ++s) {
-                    int64_t y = cy * qy + s / qx, x = cx * qx + s % qx;
-                    int kap;
-                    int el = slot_kappa(&L, rep, y, x, ctype[c], cdir[c], &kap) && kap == ckappa[c];
-                    member[c][s] = (uint8_t)el;
-                    cnt[c] += (uint64_t)el;
-                }
-                lam += cnt[c] * crate_u64[c];
-            }
-            if (lam == 0) break;                               /* quiescent cell */
-            uint32_t ctr[4] = {k, (uint32_t)gid, (uint32_t)window,
-                               (uint32_t)((window >> 32) & 0x0FFFFFFFu) | (0u << 28)};
-            uint32_t xr[4];
-            orc_philox4x32_10(ctr, key, xr);
-            /* exponential clock, eq.(totalrate): tau = -ln U / lambda */
-            uint64_t j53 = ((uint64_t)xr[0] << 21) | (uint64_t)(xr[1] >> 11);
-            double U = (double)(j53 + 1) * 0x1p-53;
-            double E = -orc_log(U);
-            double lamd = (double)lam * inv_scale;
-            double tau = E / lamd;
-            if (t + tau >= D) break;                           /* R5: pending event discarded */
-            t = t + tau;
-            /* eq.(skeleton): class with prob cnt*rate/lambda, then a uniform member site */
-            uint64_t r = (uint64_t)(((unsigned __int128)xr[2] * (unsigned __int128)lam) >> 32);
-            uint64_t cum = 0;
-            int csel = -1;
-            for (int c = 0; c < nclass; ++c) {
-                cum += cnt[c] * crate_u64[c];
-                if (cum > r) { csel = c; break; }
-            }
-            uint64_t kk = ((uint64_t)xr[3] * cnt[csel]) >> 32;
-            int ssel = -1;
-            uint64_t seen = 0;
-            for (int s = 0; s < nsite; ++s) {
-                if (member[csel][s]) {
-                    if (seen == kk) { ssel = s; break; }
-                    ++seen;
-                }
-            }
-            int64_t y = cy * qy + ssel / qx, x = cx * qx + ssel % qx;
-            apply_slot(&L, rep, y, x, ctype[csel], cdir[csel]);
-            ++k;
-        }
+        uint32_t k = cell_window(&L, rep, cy, cx, qx, qy, gid, D, window, key,
+                                 nclass, ctype, cdir, ckappa, crate_u64, inv_scale);
         if (W_events) W_events[gid] += k;
+        total += k;
+    }
+    return total;
+}
+
+/* O2 on a LIST of cells (cells[3*i] = replica, cy, cx), all of one colour: used to check sampled
+ * cells of a full-size GPU window against the pre-window lattice.  events_out[i] = events. */
+int64_t orc_window_cells(uint8_t* lat, int R, int64_t H, int64_t W, int ndim, int qx, int qy,
+                         const int64_t* cells, int64_t ncells, double D, uint64_t window, uint64_t seed,
+                         int nclass, const int* ctype, const int* cdir, const int* ckappa,
+                         const uint64_t* crate_u64, int F, uint32_t* events_out)
+{
+    latview L = {lat, H, W, ndim};
+    const int64_t Mx = W / qx, My = H / qy;
+    const double inv_scale = ldexp(1.0, -F);
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    int64_t total = 0;
+    (void)R;
+    for (int64_t i = 0; i < ncells; ++i) {
+        const int64_t rep = cells[3 * i], cy = cells[3 * i + 1], cx = cells[3 * i + 2];
+        const uint64_t gid = (uint64_t)rep * (uint64_t)(Mx * My) + (uint64_t)(cy * Mx + cx);
+        uint32_t k = cell_window(&L, rep, cy, cx, qx, qy, gid, D, window, key,
+                                 nclass, ctype, cdir, ckappa, crate_u64, inv_scale);
+        if (events_out) events_out[i] = k;
         total += k;
     }
     return total;

@@ -1,0 +1,266 @@
+"""B200-native fractional-step kinetic Monte Carlo (arXiv:1105.4673) -- Python binding.
+
+A thin ctypes layer over the C ABI of ``libkmc_b200.so`` (include/kmc.h): argument
+marshalling only.  Every step of the hot path (rate table, schedule, per-cell SSA
+windows, halo exchange, observables) runs in the library and its sm_100a kernels;
+there is no CPU fallback -- if the library is missing this module raises.
+PyTorch is used only for device memory, streams and process groups.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libkmc_b200.so")
+
+KMC_OK, KMC_EINVAL, KMC_EPARTITION, KMC_ENOMEM, KMC_ECUDA, KMC_ENCCL, KMC_ESTATE = 0, 1, 2, 3, 4, 5, 6
+KMC_WTRUNCATED = 100
+SCHEMES = {"lie": 0, "strang": 1, "random": 2}
+KINDS = {"adsdes": 0, "adsdes_diff": 1, "zgb": 2, "zgb_diff": 3}
+NSTATES = {0: 2, 1: 2, 2: 3, 3: 3}
+
+# Every symbol include/kmc.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "kmc_create", "kmc_destroy", "kmc_last_error", "kmc_create_error", "kmc_local_shape",
+    "kmc_set_config", "kmc_get_config", "kmc_set_config_device", "kmc_get_config_device",
+    "kmc_run", "kmc_substep", "kmc_observables", "kmc_get_state", "kmc_set_state",
+    "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
+    "kmc_nccl_unique_id", "kmc_version",
+]
+
+
+class KmcModel(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("ca", ctypes.c_double), ("cd", ctypes.c_double),
+                ("beta", ctypes.c_double), ("K", ctypes.c_double), ("h", ctypes.c_double),
+                ("c_hop", ctypes.c_double), ("k1", ctypes.c_double), ("k2", ctypes.c_double)]
+
+
+class KmcGeometry(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("dims", ctypes.c_int64 * 2), ("cell", ctypes.c_int32 * 2),
+                ("colours", ctypes.c_int32), ("replicas", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+
+
+class KmcDist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+
+
+class KmcObs(ctypes.Structure):
+    _fields_ = [("time", ctypes.c_double), ("windows", ctypes.c_uint64), ("events", ctypes.c_uint64),
+                ("n_state", ctypes.c_int64 * 4), ("nn_pairs", (ctypes.c_int64 * 4) * 4),
+                ("n_state_by_colour", (ctypes.c_int64 * 4) * 4), ("coverage", ctypes.c_double * 4),
+                ("energy", ctypes.c_double)]
+
+
+class KmcError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"kmc status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libkmc_b200.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() (nvcc, sm_100a)")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    vp, i32, i64, u64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    sig = {
+        "kmc_create": ([P(KmcGeometry), P(KmcModel), P(KmcDist), P(vp)], i32),
+        "kmc_destroy": ([vp], None),
+        "kmc_last_error": ([vp], ctypes.c_char_p),
+        "kmc_create_error": ([], ctypes.c_char_p),
+        "kmc_local_shape": ([vp, P(i64), P(i64), P(i64), P(i64), P(i64)], i32),
+        "kmc_set_config": ([vp, vp, i64], i32),
+        "kmc_get_config": ([vp, vp, i64], i32),
+        "kmc_set_config_device": ([vp, vp, i64], i32),
+        "kmc_get_config_device": ([vp, vp, i64], i32),
+        "kmc_run": ([vp, dbl, dbl, i32], i32),
+        "kmc_substep": ([vp, i32, dbl], i32),
+        "kmc_observables": ([vp, P(KmcObs), vp], i32),
+        "kmc_get_state": ([vp, P(u64), P(dbl)], i32),
+        "kmc_set_state": ([vp, u64, dbl], i32),
+        "kmc_rate_table": ([vp, P(i32), vp, vp, vp, vp, vp, P(i32)], i32),
+        "kmc_enable_timing": ([vp, i32], i32),
+        "kmc_timing": ([vp, P(dbl), P(i64), i32], i32),
+        "kmc_partition_plan": ([P(KmcGeometry), i32, i32, i32, vp], i32),
+        "kmc_nccl_unique_id": ([vp], i32),
+        "kmc_version": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def make_geometry(ndim, dims, cell, colours=0, replicas=1, seed=0):
+    g = KmcGeometry()
+    g.ndim = int(ndim)
+    d = list(dims) + [0] * (2 - len(dims))
+    c = list(cell) + [0] * (2 - len(cell))
+    g.dims[0], g.dims[1] = int(d[0]), int(d[1])
+    g.cell[0], g.cell[1] = int(c[0]), int(c[1])
+    g.colours = int(colours)
+    g.replicas = int(replicas)
+    g.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    return g
+
+
+def make_model(kind="adsdes", ca=1.0, cd=1.0, beta=1.0, K=0.0, h=0.0, c_hop=0.0, k1=0.4, k2=1.0):
+    m = KmcModel()
+    m.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
+    m.ca, m.cd, m.beta, m.K, m.h, m.c_hop, m.k1, m.k2 = (float(v) for v in (ca, cd, beta, K, h, c_hop, k1, k2))
+    return m
+
+
+def partition_plan(ndim, dims, cell, replicas, kind, world, rank):
+    """Host-only partition plan (kmc_partition_plan): dict of owned rows / replicas and ring neighbours."""
+    g = make_geometry(ndim, dims, cell, replicas=replicas)
+    out = (ctypes.c_int64 * 6)()
+    st = lib().kmc_partition_plan(ctypes.byref(g), KINDS[kind] if isinstance(kind, str) else int(kind),
+                                  int(world), int(rank), out)
+    if st != KMC_OK:
+        raise KmcError(st, lib().kmc_create_error().decode())
+    keys = ["replica_offset", "replicas_local", "row_offset", "rows_local", "rank_up", "rank_down"]
+    return dict(zip(keys, [int(v) for v in out]))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    st = lib().kmc_nccl_unique_id(buf)
+    if st != KMC_OK:
+        raise KmcError(st, lib().kmc_create_error().decode())
+    return bytes(buf)
+
+
+class KMC:
+    """One fractional-step KMC context (kmc_create ... kmc_destroy)."""
+
+    def __init__(self, ndim, dims, cell, kind="adsdes", colours=0, replicas=1, seed=0,
+                 rank=0, world=1, device=0, stream=None, nccl_id=None, **params):
+        self._L = lib()
+        self.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
+        self.nstates = NSTATES[self.kind]
+        self.geom = make_geometry(ndim, dims, cell, colours, replicas, seed)
+        self.model = make_model(self.kind, **params)
+        self.dist = KmcDist()
+        self.dist.rank, self.dist.world, self.dist.device = int(rank), int(world), int(device)
+        self._id = None
+        if nccl_id is not None:
+            self._id = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+            self.dist.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p)
+        self.dist.stream = stream
+        self._ctx = ctypes.c_void_p()
+        st = self._L.kmc_create(ctypes.byref(self.geom), ctypes.byref(self.model), ctypes.byref(self.dist),
+                                ctypes.byref(self._ctx))
+        if st != KMC_OK:
+            raise KmcError(st, self._L.kmc_create_error().decode())
+        rl, hl, w, ro, yo = (ctypes.c_int64() for _ in range(5))
+        self._check(self._L.kmc_local_shape(self._ctx, ctypes.byref(rl), ctypes.byref(hl), ctypes.byref(w),
+                                            ctypes.byref(ro), ctypes.byref(yo)))
+        self.local_shape = (rl.value, hl.value, w.value)
+        self.replica_offset, self.row_offset = ro.value, yo.value
+        self.nbytes = rl.value * hl.value * w.value
+
+    def _check(self, st, allow=()):
+        if st != KMC_OK and st not in allow:
+            raise KmcError(st, self._L.kmc_last_error(self._ctx).decode())
+        return st
+
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self._L.kmc_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- state -------------------------------------------------------------
+    def set_config(self, lat):
+        """Host uint8 [replicas_local][rows_local][W] (numpy) -> device (validated, synchronous)."""
+        a = np.ascontiguousarray(lat, dtype=np.uint8)
+        if a.size != self.nbytes:
+            raise ValueError(f"expected {self.nbytes} sites, got {a.size}")
+        self._check(self._L.kmc_set_config(self._ctx, a.ctypes.data, a.size))
+
+    def get_config(self):
+        out = np.empty(self.local_shape, dtype=np.uint8)
+        self._check(self._L.kmc_get_config(self._ctx, out.ctypes.data, out.size))
+        return out
+
+    def set_config_device(self, ptr, nbytes):
+        """Device uint8 buffer (e.g. torch CUDA tensor .data_ptr()), stream-ordered."""
+        self._check(self._L.kmc_set_config_device(self._ctx, ctypes.c_void_p(ptr), int(nbytes)))
+
+    def get_config_device(self, ptr, nbytes):
+        self._check(self._L.kmc_get_config_device(self._ctx, ctypes.c_void_p(ptr), int(nbytes)))
+
+    # ---- the hot path --------------------------------------------------------
+    def run(self, T, dt, scheme="lie"):
+        """kmc_run; returns True if the last macro-step was shortened (KMC_WTRUNCATED)."""
+        sc = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+        st = self._check(self._L.kmc_run(self._ctx, float(T), float(dt), sc), allow=(KMC_WTRUNCATED,))
+        return st == KMC_WTRUNCATED
+
+    def substep(self, colour, duration):
+        self._check(self._L.kmc_substep(self._ctx, int(colour), float(duration)))
+
+    def observables(self, per_cell=False):
+        o = KmcObs()
+        cells = None
+        ptr = None
+        if per_cell:
+            R, H, W = self.local_shape
+            qy = 1 if self.geom.ndim == 1 else self.geom.cell[0]
+            qx = self.geom.cell[0] if self.geom.ndim == 1 else self.geom.cell[1]
+            cells = np.zeros((R, H // qy, W // qx), dtype=np.uint32)
+            ptr = cells.ctypes.data
+        self._check(self._L.kmc_observables(self._ctx, ctypes.byref(o), ptr))
+        d = {
+            "time": o.time, "windows": int(o.windows), "events": int(o.events),
+            "n_state": np.array(o.n_state[:], dtype=np.int64),
+            "nn_pairs": np.array([o.nn_pairs[i][:] for i in range(4)], dtype=np.int64),
+            "n_state_by_colour": np.array([o.n_state_by_colour[i][:] for i in range(4)], dtype=np.int64),
+            "coverage": np.array(o.coverage[:]), "energy": o.energy,
+        }
+        if per_cell:
+            d["per_cell_events"] = cells
+        return d
+
+    def get_state(self):
+        w, t = ctypes.c_uint64(), ctypes.c_double()
+        self._check(self._L.kmc_get_state(self._ctx, ctypes.byref(w), ctypes.byref(t)))
+        return int(w.value), float(t.value)
+
+    def set_state(self, windows, time):
+        self._check(self._L.kmc_set_state(self._ctx, int(windows), float(time)))
+
+    def rate_table(self):
+        n, F = ctypes.c_int32(), ctypes.c_int32()
+        ty = (ctypes.c_int32 * 32)(); di = (ctypes.c_int32 * 32)(); ka = (ctypes.c_int32 * 32)()
+        ra = (ctypes.c_double * 32)(); ru = (ctypes.c_uint64 * 32)()
+        self._check(self._L.kmc_rate_table(self._ctx, ctypes.byref(n), ty, di, ka, ra, ru, ctypes.byref(F)))
+        k = n.value
+        return {"n": k, "type": np.array(ty[:k]), "dir": np.array(di[:k]), "kappa": np.array(ka[:k]),
+                "rate": np.array(ra[:k]), "rate_u64": np.array(ru[:k], dtype=np.uint64), "F": F.value}
+
+    # ---- timing (bench) --------------------------------------------------------
+    def enable_timing(self, on=True):
+        self._check(self._L.kmc_enable_timing(self._ctx, 1 if on else 0))
+
+    def timing(self, reset=True):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        self._check(self._L.kmc_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
+        return ms.value, n.value

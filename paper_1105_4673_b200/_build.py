@@ -1,0 +1,63 @@
+"""Build libkmc_b200.so in-tree with nvcc for sm_100a (the only target)."""
+import glob
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libkmc_b200.so")
+INCLUDE = os.path.join(ROOT, "include")
+
+
+def nccl_include() -> str:
+    try:
+        import nvidia.nccl  # torch-bundled NCCL headers (the library is dlopen'ed at run time)
+        for p in nvidia.nccl.__path__:
+            inc = os.path.join(p, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except ImportError:
+        pass
+    for inc in ("/usr/include", "/usr/local/cuda/include"):
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    raise RuntimeError("nccl.h not found")
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def deps():
+    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(INCLUDE, "kmc.h"), __file__]
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    return all(os.path.getmtime(d) <= t for d in deps())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return LIB
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared",
+           "-I", INCLUDE, "-I", nccl_include(), "-Xptxas", "-v" if verbose else "-O3",
+           "-o", LIB + ".tmp"] + sources() + ["-ldl"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libkmc_b200.so")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose="-v" in sys.argv))

@@ -1,0 +1,702 @@
+// kmc_capi.cu -- host runtime and C ABI of libkmc_b200.so (declared in include/kmc.h).
+//
+// Owns: validation of the geometry (R6/R7), the rate table a1 (eq.(Arrhenius) P:963-968,
+// Table COrates, R12-R14, quantised per R18), the schedule a2 (eq.(lie) P:395-401,
+// eq.(strang), eq.(SLPCS); R1-R4, R20), the stream-ordered sub-step loop, the
+// multi-GPU slab decomposition with its NCCL halo exchange a7 and the
+// observables a8.  Product code; shares nothing with oracle/.
+#include "kmc_internal.h"
+#include "../../include/kmc.h"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <dlfcn.h>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+using namespace kmc;
+
+#define KMC_VERSION "kmc_b200 0.1 (sm_100a)"
+
+// ---------------------------------------------------------------------------------------------
+// NCCL, loaded lazily with dlopen so the library loads on machines without it (world = 1).
+// ---------------------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+bool load_nccl(std::string* why) {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.tried) { if (!g_nccl.ok && why) *why = g_nccl.err; return g_nccl.ok; }
+    g_nccl.tried = true;
+    const char* env = getenv("KMC_NCCL_LIB");
+    void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { g_nccl.err = std::string("dlopen libnccl.so.2 failed: ") + dlerror(); if (why) *why = g_nccl.err; return false; }
+#define LOADSYM(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+    if (!g_nccl.field) { g_nccl.err = std::string("missing NCCL symbol ") + name; if (why) *why = g_nccl.err; return false; }
+    LOADSYM(GetUniqueId, "ncclGetUniqueId");
+    LOADSYM(CommInitRank, "ncclCommInitRank");
+    LOADSYM(CommDestroy, "ncclCommDestroy");
+    LOADSYM(Send, "ncclSend");
+    LOADSYM(Recv, "ncclRecv");
+    LOADSYM(GroupStart, "ncclGroupStart");
+    LOADSYM(GroupEnd, "ncclGroupEnd");
+    LOADSYM(AllReduce, "ncclAllReduce");
+    LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+    g_nccl.ok = true;
+    return true;
+}
+
+std::string g_create_error;
+
+// Philox4x32-10 on the host (random schedule, R4).
+void philox_host(uint32_t c[4], uint32_t k0, uint32_t k1) {
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        c[1] = (uint32_t)p1;
+        c[3] = (uint32_t)p0;
+        c[0] = n0;
+        c[2] = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+}  // namespace
+
+struct kmc_ctx {
+    kmc_geometry geom{};
+    kmc_model model{};
+    int rank = 0, world = 1, device = 0;
+    int kind = 0, nplanes = 1, nstates = 2, C = 2;
+    bool cross = false;             // events write outside the anchor cell
+    Geo g{};
+    long long H_local = 0, W = 0;
+    // rate table
+    int nclass = 0, F = 0;
+    int ctype[kMaxClass], cdir[kMaxClass], ckappa[kMaxClass];
+    double crate[kMaxClass];
+    uint64_t crate_u64[kMaxClass];
+    // device state
+    uint64_t* planes[2] = {nullptr, nullptr};
+    long long plane_words = 0;
+    uint32_t* wev = nullptr;
+    unsigned long long* ev_total = nullptr;
+    unsigned long long* obs_buf = nullptr;   // kObsCounters + 1 (events)
+    unsigned int* err_flag = nullptr;
+    uint8_t* staging = nullptr;              // uint8 local slab (set/get_config from host)
+    uint64_t* ghost_snap = nullptr;          // [2 rows][nplanes] snapshot / delta buffers (world > 1)
+    uint64_t* ghost_recv = nullptr;
+    unsigned long long* h_obs = nullptr;     // pinned
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // schedule state
+    uint64_t window = 0;
+    double time = 0.0;
+    // timing
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+    size_t tev_used = 0;
+    // multi-GPU
+    ncclComm_t comm = nullptr;
+    int rank_up = -1, rank_down = -1;        // -y and +y ring neighbours (2D slabs)
+    std::string err;
+};
+
+namespace {
+
+kmc_status fail(kmc_ctx* c, kmc_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf; else g_create_error = buf;
+    return s;
+}
+
+#define CUDA_TRY(ctx, call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) \
+    return fail(ctx, KMC_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); } while (0)
+#define NCCL_TRY(ctx, call) do { ncclResult_t r_ = (call); if (r_ != ncclSuccess) \
+    return fail(ctx, KMC_ENCCL, "%s: %s", #call, g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "?"); } while (0)
+
+int types_per_site(int kind, int z) {
+    switch (kind) {
+    case KMC_ADSDES: return 2;
+    case KMC_ADSDES_DIFF: return 2 + z;
+    case KMC_ZGB: return 1 + 3 * z;
+    case KMC_ZGB_DIFF: return 1 + 4 * z;
+    }
+    return 0;
+}
+
+// a1: class list in canonical order with FP64 rates.
+int build_classes(const kmc_model& m, int ndim, int* type, int* dir, int* kappa, double* rate) {
+    const int z = 2 * ndim;
+    int n = 0;
+    auto add = [&](int t, int d, int k, double r) { type[n] = t; dir[n] = d; kappa[n] = k; rate[n] = r; ++n; };
+    if (m.kind == KMC_ADSDES || m.kind == KMC_ADSDES_DIFF) {
+        add(T_ADS, -1, 0, m.ca);                                   // c1 (1 - sigma)
+        for (int nn = 0; nn <= z; ++nn) {                          // c2 sigma exp(-beta U), U = K n + h
+            double u = m.K * (double)nn;
+            u = u + m.h;
+            u = m.beta * u;
+            u = -u;
+            add(T_DES, -1, nn, m.cd * std::exp(u));
+        }
+        if (m.kind == KMC_ADSDES_DIFF)
+            for (int d = 0; d < z; ++d)
+                for (int nn = 0; nn < z; ++nn) {                   // R12: c_hop exp(-beta K n(x))
+                    double u = m.K * (double)nn;
+                    u = m.beta * u;
+                    u = -u;
+                    add(T_HOP, d, nn, m.c_hop * std::exp(u));
+                }
+        return n;
+    }
+    add(T_COADS, -1, 0, m.k1);
+    for (int d = 0; d < z; ++d) add(T_O2ADS, d, 0, (1.0 - m.k1) / (double)z);
+    for (int d = 0; d < z; ++d) add(T_RCO, d, 0, m.k2 / (double)z);
+    for (int d = 0; d < z; ++d) add(T_RO, d, 0, m.k2 / (double)z);
+    if (m.kind == KMC_ZGB_DIFF)
+        for (int d = 0; d < z; ++d) add(T_COHOP, d, 0, m.c_hop);
+    return n;
+}
+
+// R18 quantisation; returns F or -1.
+int quantise(const double* rate, int n, long long slots_bound, uint64_t* out) {
+    double rmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+        if (!(rate[i] >= 0.0) || std::isinf(rate[i])) return -1;
+        rmax = rate[i] > rmax ? rate[i] : rmax;
+    }
+    int F = 0;
+    if (rmax > 0.0) {
+        int e = 0;
+        const double mant = std::frexp(rmax * (double)slots_bound, &e);
+        const int ceil_log2 = (mant == 0.5) ? e - 1 : e;
+        F = 62 - ceil_log2;
+        if (F < 0) return -1;
+    }
+    for (int i = 0; i < n; ++i) out[i] = (uint64_t)std::llround(std::ldexp(rate[i], F));
+    return F;
+}
+
+uint64_t lowmask(int nbits) { return nbits >= 64 ? ~0ull : ((1ull << nbits) - 1ull); }
+
+long long active_cells(const kmc_ctx* c) {
+    const long long half = c->g.Mx / 2;
+    if (c->g.ndim == 1) return half * c->g.R;
+    const long long rows = (c->C == 2) ? c->g.My_local : c->g.My_local / 2;
+    return half * c->g.R * rows;
+}
+
+// a7 forward exchange (world > 1, 2D): owned boundary cell rows -> neighbours' ghost rows.
+kmc_status exchange_forward(kmc_ctx* c) {
+    if (c->world == 1 || c->g.ndim == 1) return KMC_OK;
+    const size_t rowlen = (size_t)c->g.R * c->g.Mx;
+    const int My = c->g.My_local;
+    NCCL_TRY(c, g_nccl.GroupStart());
+    for (int p = 0; p < c->nplanes; ++p) {
+        uint64_t* pl = c->planes[p];
+        // order matters when rank_up == rank_down (world = 2): last row first, then first row
+        NCCL_TRY(c, g_nccl.Send(pl + (size_t)My * rowlen, rowlen * 8, ncclUint8, c->rank_down, c->comm, c->stream));
+        NCCL_TRY(c, g_nccl.Send(pl + rowlen, rowlen * 8, ncclUint8, c->rank_up, c->comm, c->stream));
+        NCCL_TRY(c, g_nccl.Recv(pl, rowlen * 8, ncclUint8, c->rank_up, c->comm, c->stream));
+        NCCL_TRY(c, g_nccl.Recv(pl + (size_t)(My + 1) * rowlen, rowlen * 8, ncclUint8, c->rank_down, c->comm, c->stream));
+    }
+    NCCL_TRY(c, g_nccl.GroupEnd());
+    if (c->cross) {   // snapshot the ghost rows so the sub-step's writes into them can be sent back
+        for (int p = 0; p < c->nplanes; ++p) {
+            CUDA_TRY(c, cudaMemcpyAsync(c->ghost_snap + (size_t)(2 * p) * rowlen, c->planes[p], rowlen * 8,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_TRY(c, cudaMemcpyAsync(c->ghost_snap + (size_t)(2 * p + 1) * rowlen, c->planes[p] + (size_t)(My + 1) * rowlen,
+                                        rowlen * 8, cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
+    return KMC_OK;
+}
+
+// a7 reverse exchange for cross-cell-writing models: ghost-row deltas back to their owners,
+// merged by XOR (same-colour closures are disjoint, R6, so exactly one writer per bit).
+kmc_status exchange_reverse(kmc_ctx* c) {
+    if (c->world == 1 || c->g.ndim == 1 || !c->cross) return KMC_OK;
+    const size_t rowlen = (size_t)c->g.R * c->g.Mx;
+    const int My = c->g.My_local;
+    for (int p = 0; p < c->nplanes; ++p) {   // snap := ghost XOR snap  (the delta)
+        CUDA_TRY(c, launch_xor_rows(c->ghost_snap + (size_t)(2 * p) * rowlen, c->planes[p], nullptr, (long long)rowlen, c->stream));
+        CUDA_TRY(c, launch_xor_rows(c->ghost_snap + (size_t)(2 * p + 1) * rowlen, c->planes[p] + (size_t)(My + 1) * rowlen,
+                                    nullptr, (long long)rowlen, c->stream));
+    }
+    NCCL_TRY(c, g_nccl.GroupStart());
+    for (int p = 0; p < c->nplanes; ++p) {
+        // send: top-ghost delta -> up (its last row), bottom-ghost delta -> down (its first row)
+        NCCL_TRY(c, g_nccl.Send(c->ghost_snap + (size_t)(2 * p) * rowlen, rowlen * 8, ncclUint8, c->rank_up, c->comm, c->stream));
+        NCCL_TRY(c, g_nccl.Send(c->ghost_snap + (size_t)(2 * p + 1) * rowlen, rowlen * 8, ncclUint8, c->rank_down, c->comm, c->stream));
+        // receive (same per-peer order as the peer's sends): delta for my last row from down, first row from up
+        NCCL_TRY(c, g_nccl.Recv(c->ghost_recv + (size_t)(2 * p + 1) * rowlen, rowlen * 8, ncclUint8, c->rank_down, c->comm, c->stream));
+        NCCL_TRY(c, g_nccl.Recv(c->ghost_recv + (size_t)(2 * p) * rowlen, rowlen * 8, ncclUint8, c->rank_up, c->comm, c->stream));
+    }
+    NCCL_TRY(c, g_nccl.GroupEnd());
+    for (int p = 0; p < c->nplanes; ++p) {
+        CUDA_TRY(c, launch_xor_rows(c->planes[p] + rowlen, c->ghost_recv + (size_t)(2 * p) * rowlen, nullptr,
+                                    (long long)rowlen, c->stream));
+        CUDA_TRY(c, launch_xor_rows(c->planes[p] + (size_t)My * rowlen, c->ghost_recv + (size_t)(2 * p + 1) * rowlen,
+                                    nullptr, (long long)rowlen, c->stream));
+    }
+    return KMC_OK;
+}
+
+kmc_status do_substep(kmc_ctx* c, int colour, double D) {
+    if (colour < 0 || colour >= c->C) return fail(c, KMC_EINVAL, "colour %d out of range [0,%d)", colour, c->C);
+    if (!(D >= 0.0)) return fail(c, KMC_EINVAL, "window duration must be >= 0");
+    kmc_status st = exchange_forward(c);
+    if (st != KMC_OK) return st;
+    SubstepArgs a{};
+    a.g = c->g;
+    a.plane0 = c->planes[0];
+    a.plane1 = c->planes[1];
+    a.wev = c->wev;
+    a.ev_total = c->ev_total;
+    a.colour = colour;
+    a.C = c->C;
+    a.D = D;
+    a.inv_scale = std::ldexp(1.0, -c->F);
+    a.key0 = (uint32_t)c->geom.seed;
+    a.key1 = (uint32_t)(c->geom.seed >> 32);
+    a.w_lo = (uint32_t)c->window;
+    a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
+    for (int i = 0; i < c->nclass; ++i) a.rate[i] = c->crate_u64[i];
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        if (c->tev_used == c->tev.size()) {
+            cudaEvent_t x, y;
+            CUDA_TRY(c, cudaEventCreate(&x));
+            CUDA_TRY(c, cudaEventCreate(&y));
+            c->tev.emplace_back(x, y);
+        }
+        e0 = c->tev[c->tev_used].first;
+        e1 = c->tev[c->tev_used].second;
+        ++c->tev_used;
+        CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+    }
+    CUDA_TRY(c, launch_substep(c->kind, a, active_cells(c), c->stream));
+    if (c->timing) CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+    c->window += 1;
+    return exchange_reverse(c);
+}
+
+int random_colour(uint64_t seed, uint64_t w, int C) {
+    uint32_t ctr[4] = {0u, 0u, (uint32_t)w, (uint32_t)((w >> 32) & 0x0FFFFFFFu) | (1u << 28)};   // tag SCHED
+    philox_host(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
+    return (int)(((uint64_t)C * ctr[0]) >> 32);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* kmc_version(void) { return KMC_VERSION; }
+const char* kmc_create_error(void) { return g_create_error.c_str(); }
+const char* kmc_last_error(const kmc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
+
+kmc_status kmc_partition_plan(const kmc_geometry* geom, int32_t kind, int32_t world, int32_t rank, int64_t out[6]) {
+    if (!geom || !out || world < 1 || rank < 0 || rank >= world) return fail(nullptr, KMC_EINVAL, "bad partition arguments");
+    const bool cross = kind != KMC_ADSDES;
+    if (geom->ndim == 1) {
+        if (geom->replicas % world) return fail(nullptr, KMC_EPARTITION, "1D: replicas %d not divisible by world %d", geom->replicas, world);
+        const int64_t rl = geom->replicas / world;
+        out[0] = rank * rl; out[1] = rl; out[2] = 0; out[3] = 1; out[4] = -1; out[5] = -1;
+        return KMC_OK;
+    }
+    const int64_t H = geom->dims[0];
+    const int qy = geom->cell[0];
+    if (qy <= 0 || H % ((int64_t)world * 2 * qy))
+        return fail(nullptr, KMC_EPARTITION, "2D: rows %lld not a multiple of world*2*q_y = %lld", (long long)H,
+                    (long long)world * 2 * qy);
+    const int64_t rows_cells = H / qy / world;
+    out[0] = 0; out[1] = geom->replicas; out[2] = rank * rows_cells; out[3] = rows_cells;
+    out[4] = world > 1 ? (rank + world - 1) % world : -1;
+    out[5] = world > 1 ? (rank + 1) % world : -1;
+    (void)cross;
+    return KMC_OK;
+}
+
+kmc_status kmc_nccl_unique_id(uint8_t out[128]) {
+    std::string why;
+    if (!out) return fail(nullptr, KMC_EINVAL, "NULL out");
+    if (!load_nccl(&why)) return fail(nullptr, KMC_ENCCL, "%s", why.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, KMC_ENCCL, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out, &id, 128);
+    return KMC_OK;
+}
+
+kmc_status kmc_create(const kmc_geometry* geom, const kmc_model* model, const kmc_dist* dist, kmc_ctx** out) {
+    if (!out) return fail(nullptr, KMC_EINVAL, "NULL out");
+    *out = nullptr;
+    if (!geom || !model) return fail(nullptr, KMC_EINVAL, "NULL geometry or model");
+    if (model->kind < 0 || model->kind > 3) return fail(nullptr, KMC_EINVAL, "unknown model kind %d", model->kind);
+    if (geom->ndim != 1 && geom->ndim != 2) return fail(nullptr, KMC_EINVAL, "ndim must be 1 or 2");
+    if (geom->replicas < 1) return fail(nullptr, KMC_EINVAL, "replicas must be >= 1");
+    const int world = dist ? dist->world : 1, rank = dist ? dist->rank : 0;
+    if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, KMC_EINVAL, "bad rank/world");
+
+    const int ndim = geom->ndim;
+    const long long H = ndim == 1 ? 1 : geom->dims[0];
+    const long long W = ndim == 1 ? geom->dims[0] : geom->dims[1];
+    const int qy = ndim == 1 ? 1 : geom->cell[0];
+    const int qx = ndim == 1 ? geom->cell[0] : geom->cell[1];
+    const bool cross = model->kind != KMC_ADSDES;
+    if (H < 1 || W < 1 || qx < 1 || qy < 1) return fail(nullptr, KMC_EINVAL, "dims and cell must be positive");
+    if (qx * qy > 64) return fail(nullptr, KMC_EPARTITION, "cell has %d sites (> 64)", qx * qy);
+    if (W % qx || H % qy) return fail(nullptr, KMC_EPARTITION, "dims not divisible by the cell");
+    const long long Mx = W / qx, My = H / qy;
+    if (Mx % 2 || (ndim == 2 && My % 2)) return fail(nullptr, KMC_EPARTITION, "need an even number of cells per axis");
+    if (cross && (qx < 2 || (ndim == 2 && qy < 2)))
+        return fail(nullptr, KMC_EPARTITION, "cross-cell-writing model needs cell extent >= 2 (R7)");
+    int C = geom->colours;
+    if (C == 0) C = (ndim == 1 || !cross) ? 2 : 4;
+    if (C != 2 && C != 4) return fail(nullptr, KMC_EPARTITION, "colours must be 2 or 4");
+    if (ndim == 1 && C != 2) return fail(nullptr, KMC_EPARTITION, "1D lattices use 2 colours");
+    if (ndim == 2 && cross && C == 2)
+        return fail(nullptr, KMC_EPARTITION, "2D model with cross-cell writes needs 4 colours (R6)");
+    if ((long long)geom->replicas * Mx * My > 0xFFFFFFFFLL)
+        return fail(nullptr, KMC_EPARTITION, "more than 2^32 cells in total (Philox counter word)");
+    int64_t plan[6];
+    kmc_status ps = kmc_partition_plan(geom, model->kind, world, rank, plan);
+    if (ps != KMC_OK) return ps;
+
+    kmc_ctx* c = new kmc_ctx();
+    c->geom = *geom;
+    c->model = *model;
+    c->rank = rank; c->world = world; c->device = dist ? dist->device : 0;
+    c->kind = model->kind;
+    c->nplanes = (model->kind >= KMC_ZGB) ? 2 : 1;
+    c->nstates = c->nplanes + 1;
+    c->C = C;
+    c->cross = cross;
+    c->W = W;
+    Geo& g = c->g;
+    g.ndim = ndim; g.qx = qx; g.qy = qy; g.nsite = qx * qy;
+    g.Mx = (int)Mx;
+    g.R = (int)plan[1];
+    g.rep_offset = (int)plan[0];
+    g.row_offset = (int)plan[2];
+    g.My_local = (int)plan[3];
+    g.ghost = (world > 1 && ndim == 2) ? 1 : 0;
+    g.M_global = Mx * My;
+    g.shN = qx * (qy - 1);
+    g.valid = lowmask(qx * qy);
+    g.col0 = 0; g.colL = 0;
+    for (int y = 0; y < qy; ++y) { g.col0 |= 1ull << (y * qx); g.colL |= 1ull << (y * qx + qx - 1); }
+    g.row0 = lowmask(qx);
+    g.rowL = g.row0 << g.shN;
+    c->H_local = (long long)g.My_local * qy;
+    c->rank_up = (int)plan[4];
+    c->rank_down = (int)plan[5];
+
+    // a1: the rate table
+    c->nclass = build_classes(*model, ndim, c->ctype, c->cdir, c->ckappa, c->crate);
+    c->F = quantise(c->crate, c->nclass, (long long)g.nsite * types_per_site(c->kind, 2 * ndim), c->crate_u64);
+    if (c->F < 0) { delete c; return fail(nullptr, KMC_EINVAL, "rates must be finite and >= 0 (and quantisable)"); }
+
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) { delete c; return fail(nullptr, KMC_ECUDA, "cudaSetDevice(%d): %s", dist ? dist->device : 0, cudaGetErrorString(e)); }
+    if (dist && dist->stream) c->stream = (cudaStream_t)dist->stream;
+    else {
+        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { delete c; return fail(nullptr, KMC_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
+        c->own_stream = true;
+    }
+    const long long rows_storage = g.My_local + 2 * g.ghost;
+    c->plane_words = rows_storage * (long long)g.R * g.Mx;
+    const long long owned = (long long)g.My_local * g.R * g.Mx;
+    auto alloc = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
+    bool ok = true;
+    for (int p = 0; p < c->nplanes; ++p) ok = ok && alloc((void**)&c->planes[p], (size_t)c->plane_words * 8);
+    ok = ok && alloc((void**)&c->wev, (size_t)owned * 4);
+    ok = ok && alloc((void**)&c->ev_total, 8);
+    ok = ok && alloc((void**)&c->obs_buf, (kObsCounters + 1) * 8);
+    ok = ok && alloc((void**)&c->err_flag, 4);
+    if (g.ghost) {
+        ok = ok && alloc((void**)&c->ghost_snap, (size_t)4 * g.R * g.Mx * 8);
+        ok = ok && alloc((void**)&c->ghost_recv, (size_t)4 * g.R * g.Mx * 8);
+    }
+    ok = ok && cudaMallocHost((void**)&c->h_obs, (kObsCounters + 1) * 8) == cudaSuccess;
+    if (!ok) { kmc_destroy(c); return fail(nullptr, KMC_ENOMEM, "device allocation failed (%lld words)", c->plane_words); }
+    for (int p = 0; p < c->nplanes; ++p) cudaMemsetAsync(c->planes[p], 0, (size_t)c->plane_words * 8, c->stream);
+    cudaMemsetAsync(c->wev, 0, (size_t)owned * 4, c->stream);
+    cudaMemsetAsync(c->ev_total, 0, 8, c->stream);
+    e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) { kmc_destroy(c); return fail(nullptr, KMC_ECUDA, "init: %s", cudaGetErrorString(e)); }
+
+    if (world > 1) {
+        std::string why;
+        if (!dist->nccl_unique_id) { kmc_destroy(c); return fail(nullptr, KMC_EINVAL, "world > 1 needs nccl_unique_id"); }
+        if (!load_nccl(&why)) { kmc_destroy(c); return fail(nullptr, KMC_ENCCL, "%s", why.c_str()); }
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_unique_id, 128);
+        ncclResult_t r = g_nccl.CommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) { kmc_destroy(c); return fail(nullptr, KMC_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)); }
+    }
+    *out = c;
+    return KMC_OK;
+}
+
+void kmc_destroy(kmc_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+    for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
+    cudaFree(c->wev); cudaFree(c->ev_total); cudaFree(c->obs_buf); cudaFree(c->err_flag);
+    cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv);
+    if (c->h_obs) cudaFreeHost(c->h_obs);
+    for (auto& pr : c->tev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+kmc_status kmc_local_shape(const kmc_ctx* c, int64_t* rl, int64_t* hl, int64_t* w, int64_t* ro, int64_t* yo) {
+    if (!c) return KMC_EINVAL;
+    if (rl) *rl = c->g.R;
+    if (hl) *hl = c->H_local;
+    if (w) *w = c->W;
+    if (ro) *ro = c->g.rep_offset;
+    if (yo) *yo = (int64_t)c->g.row_offset * c->g.qy;
+    return KMC_OK;
+}
+
+static long long slab_bytes(const kmc_ctx* c) { return (long long)c->g.R * c->H_local * c->W; }
+
+static kmc_status ensure_staging(kmc_ctx* c) {
+    if (c->staging) return KMC_OK;
+    if (cudaMalloc((void**)&c->staging, (size_t)slab_bytes(c)) != cudaSuccess)
+        return fail(c, KMC_ENOMEM, "staging allocation of %lld bytes failed", slab_bytes(c));
+    return KMC_OK;
+}
+
+kmc_status kmc_set_config_device(kmc_ctx* c, const uint8_t* dev, int64_t nbytes) {
+    if (!c || !dev) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, launch_pack(c->g, dev, c->planes[0], c->nplanes > 1 ? c->planes[1] : nullptr, c->nstates, c->err_flag, c->stream));
+    return KMC_OK;
+}
+
+kmc_status kmc_get_config_device(kmc_ctx* c, uint8_t* dev, int64_t nbytes) {
+    if (!c || !dev) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, launch_unpack(c->g, c->planes[0], c->planes[1], c->nplanes, dev, c->stream));
+    return KMC_OK;
+}
+
+kmc_status kmc_set_config(kmc_ctx* c, const uint8_t* host, int64_t nbytes) {
+    if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
+    kmc_status st = ensure_staging(c);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    // validate in a scratch copy of the planes so an invalid slab leaves the lattice unchanged
+    CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->staging, host, (size_t)nbytes, cudaMemcpyHostToDevice, c->stream));
+    uint64_t* tmp[2] = {nullptr, nullptr};
+    for (int p = 0; p < c->nplanes; ++p) CUDA_TRY(c, cudaMallocAsync((void**)&tmp[p], (size_t)c->plane_words * 8, c->stream));
+    CUDA_TRY(c, launch_pack(c->g, c->staging, tmp[0], tmp[1], c->nstates, c->err_flag, c->stream));
+    unsigned bad = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&bad, c->err_flag, 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (!bad)
+        for (int p = 0; p < c->nplanes; ++p) std::swap(tmp[p], c->planes[p]);
+    for (int p = 0; p < c->nplanes; ++p) CUDA_TRY(c, cudaFreeAsync(tmp[p], c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (bad) return fail(c, KMC_EINVAL, "spin value >= %d in the configuration", c->nstates);
+    return KMC_OK;
+}
+
+kmc_status kmc_get_config(kmc_ctx* c, uint8_t* host, int64_t nbytes) {
+    if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
+    kmc_status st = ensure_staging(c);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, launch_unpack(c->g, c->planes[0], c->planes[1], c->nplanes, c->staging, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(host, c->staging, (size_t)nbytes, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return KMC_OK;
+}
+
+kmc_status kmc_substep(kmc_ctx* c, int32_t colour, double duration) {
+    if (!c) return KMC_EINVAL;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return do_substep(c, colour, duration);
+}
+
+kmc_status kmc_run(kmc_ctx* c, double T, double dt, kmc_scheme scheme) {
+    if (!c) return KMC_EINVAL;
+    if (!(dt > 0.0) || !(T >= 0.0) || std::isinf(T)) return fail(c, KMC_EINVAL, "need dt > 0 and finite T >= 0");
+    if (scheme < KMC_LIE || scheme > KMC_RANDOM) return fail(c, KMC_EINVAL, "unknown scheme %d", (int)scheme);
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (T == 0.0) return KMC_OK;
+    // R20: n = ceil(T/dt - 1e-9) macro-steps, the last of duration T - (n-1) dt
+    long long n = (long long)std::ceil(T / dt - 1e-9);
+    if (n < 1) n = 1;
+    double last = T - (double)(n - 1) * dt;
+    bool truncated = true;
+    if (std::fabs(last - dt) <= 1e-9 * dt) { last = dt; truncated = false; }
+    for (long long i = 0; i < n; ++i) {
+        const double d = (i == n - 1) ? last : dt;
+        const double h = d * 0.5;
+        kmc_status st = KMC_OK;
+        if (scheme == KMC_LIE) {                       // eq.(lie), colour 0 first (R1)
+            for (int col = 0; col < c->C && st == KMC_OK; ++col) st = do_substep(c, col, d);
+        } else if (scheme == KMC_STRANG) {             // eq.(strang), halves to colour 0 (R2)
+            if (c->C == 2) {
+                const int cs[3] = {0, 1, 0};
+                const double ds[3] = {h, d, h};
+                for (int k = 0; k < 3 && st == KMC_OK; ++k) st = do_substep(c, cs[k], ds[k]);
+            } else {
+                const int cs[7] = {0, 1, 2, 3, 2, 1, 0};
+                const double ds[7] = {h, h, h, d, h, h, h};
+                for (int k = 0; k < 7 && st == KMC_OK; ++k) st = do_substep(c, cs[k], ds[k]);
+            }
+        } else {                                       // eq.(SLPCS): C windows, xi_w by window id (R4)
+            for (int k = 0; k < c->C && st == KMC_OK; ++k) st = do_substep(c, random_colour(c->geom.seed, c->window, c->C), d);
+        }
+        if (st != KMC_OK) return st;
+        c->time += d;
+    }
+    return truncated ? KMC_WTRUNCATED : KMC_OK;
+}
+
+kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
+    if (!c || !o) return fail(c, KMC_EINVAL, "NULL argument");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st = exchange_forward(c);   // ghosts current for the +y bonds of the last owned row
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c, cudaMemsetAsync(c->obs_buf, 0, kObsCounters * 8, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->obs_buf + kObsCounters, c->ev_total, 8, cudaMemcpyDeviceToDevice, c->stream));
+    ObsArgs a{};
+    a.g = c->g;
+    a.plane0 = c->planes[0];
+    a.plane1 = c->planes[1];
+    a.nplanes = c->nplanes;
+    a.C = c->C;
+    a.out = c->obs_buf;
+    CUDA_TRY(c, launch_observables(a, c->stream));
+    if (c->world > 1)
+        NCCL_TRY(c, g_nccl.AllReduce(c->obs_buf, c->obs_buf, kObsCounters + 1, ncclUint64, ncclSum, c->comm, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_obs, c->obs_buf, (kObsCounters + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<uint32_t> wl;
+    const long long owned = (long long)c->g.My_local * c->g.R * c->g.Mx;
+    if (per_cell) {
+        wl.resize((size_t)owned);
+        CUDA_TRY(c, cudaMemcpyAsync(wl.data(), c->wev, (size_t)owned * 4, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const unsigned long long* h = c->h_obs;
+    memset(o, 0, sizeof *o);
+    o->time = c->time;
+    o->windows = c->window;
+    o->events = h[kObsCounters];
+    long long total = 0;
+    for (int s = 0; s < 4; ++s) { o->n_state[s] = (int64_t)h[s]; total += (long long)h[s]; }
+    for (int col = 0; col < 4; ++col)
+        for (int s = 0; s < 4; ++s) o->n_state_by_colour[col][s] = (int64_t)h[4 + col * 4 + s];
+    for (int a2 = 0; a2 < 4; ++a2)
+        for (int b = a2; b < 4; ++b) {
+            int64_t v = (int64_t)h[20 + a2 * 4 + b];
+            if (b != a2) v += (int64_t)h[20 + b * 4 + a2];
+            o->nn_pairs[a2][b] = o->nn_pairs[b][a2] = v;
+        }
+    for (int s = 0; s < 4; ++s) o->coverage[s] = total ? (double)o->n_state[s] / (double)total : 0.0;
+    o->energy = -c->model.K * (double)o->nn_pairs[1][1] + c->model.h * (double)o->n_state[1];   // R24
+    if (per_cell) {   // device order [cy][r][cx] -> [r][cy][cx]
+        const int R = c->g.R, My = c->g.My_local, Mx = c->g.Mx;
+        for (int cy = 0; cy < My; ++cy)
+            for (int r = 0; r < R; ++r)
+                memcpy(per_cell + ((size_t)r * My + cy) * Mx, wl.data() + ((size_t)cy * R + r) * Mx, (size_t)Mx * 4);
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_get_state(const kmc_ctx* c, uint64_t* windows, double* time) {
+    if (!c) return KMC_EINVAL;
+    if (windows) *windows = c->window;
+    if (time) *time = c->time;
+    return KMC_OK;
+}
+
+kmc_status kmc_set_state(kmc_ctx* c, uint64_t windows, double time) {
+    if (!c) return KMC_EINVAL;
+    c->window = windows;
+    c->time = time;
+    return KMC_OK;
+}
+
+kmc_status kmc_rate_table(const kmc_ctx* c, int32_t* n, int32_t* type, int32_t* dir, int32_t* kappa,
+                          double* rate, uint64_t* rate_u64, int32_t* F) {
+    if (!c) return KMC_EINVAL;
+    if (n) *n = c->nclass;
+    if (F) *F = c->F;
+    for (int i = 0; i < c->nclass; ++i) {
+        if (type) type[i] = c->ctype[i];
+        if (dir) dir[i] = c->cdir[i];
+        if (kappa) kappa[i] = c->ckappa[i];
+        if (rate) rate[i] = c->crate[i];
+        if (rate_u64) rate_u64[i] = c->crate_u64[i];
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_enable_timing(kmc_ctx* c, int32_t enable) {
+    if (!c) return KMC_EINVAL;
+    c->timing = enable != 0;
+    return KMC_OK;
+}
+
+kmc_status kmc_timing(kmc_ctx* c, double* kernel_ms, int64_t* launches, int32_t reset) {
+    if (!c) return KMC_EINVAL;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    double tot = 0.0;
+    for (size_t i = 0; i < c->tev_used; ++i) {
+        float ms = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, c->tev[i].first, c->tev[i].second));
+        tot += ms;
+    }
+    if (kernel_ms) *kernel_ms = tot;
+    if (launches) *launches = (int64_t)c->tev_used;
+    if (reset) c->tev_used = 0;
+    return KMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// kmc_internal.h -- shared declarations of the CUDA kernels and the host runtime of
+// libkmc_b200.so.  Product code; shares nothing with oracle/.
+//
+// Data layout in HBM: the lattice is bit-packed CELL-MAJOR.  One uint64 word
+// holds one coarse cell (q_x*q_y <= 64 sites, local site s = ly*q_x + lx, bit s) of one bit-plane:
+//   adsdes*:  plane 0 = occupied
+//   zgb*:     plane 0 = CO, plane 1 = O        (vacant = neither)
+// Words are stored [plane][storage row sy][replica r][cell column cx]; storage rows are the
+// rank's owned cell rows, plus one ghost cell row above (sy = 0) and below (sy = My_local+1)
+// when a 2D lattice is split over ranks (ghost = 1).  A row across all replicas is contiguous,
+// so a halo exchange moves one contiguous block per plane.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kmc {
+
+constexpr int kMaxClass = 32;
+
+// Slot types, used by the host rate table.
+enum SlotType { T_ADS = 0, T_DES = 1, T_HOP = 2, T_COADS = 3, T_O2ADS = 4, T_RCO = 5, T_RO = 6, T_COHOP = 7 };
+
+struct Geo {
+    int ndim, qx, qy, nsite;
+    int Mx, My_local, R, ghost;      // cells per row, owned cell rows, replicas (local), ghost rows?
+    int row_offset;                  // global cell row of owned row 0
+    int rep_offset;                  // global replica of local replica 0
+    long long M_global;              // cells per replica (global)
+    int shN;                         // q_x*(q_y-1): bit offset of the last row
+    uint64_t valid, col0, colL, row0, rowL;
+};
+
+struct SubstepArgs {
+    Geo g;
+    uint64_t* plane0;
+    uint64_t* plane1;
+    uint32_t* wev;                   // cumulative events per owned cell [My_local][R][Mx]
+    unsigned long long* ev_total;    // device event counter
+    int colour, C;
+    double D;                        // window duration
+    double inv_scale;                // 2^-F
+    uint32_t key0, key1;             // Philox key = seed
+    uint32_t w_lo, w_hi_tag;         // window id (tag EVT = 0 in bits 28..31)
+    uint64_t rate[kMaxClass];        // u64 fixed-point class rates (R18)
+};
+
+struct ObsArgs {
+    Geo g;
+    const uint64_t* plane0;
+    const uint64_t* plane1;
+    int nplanes, C;
+    unsigned long long* out;         // [4 n_state][16 by_colour][16 nn ordered]
+};
+
+constexpr int kObsCounters = 4 + 16 + 16;
+
+// kernels.cu
+cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cudaStream_t s);
+cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s);
+cudaError_t launch_pack(const Geo& g, const uint8_t* in, uint64_t* p0, uint64_t* p1, int nstates,
+                        unsigned int* err, cudaStream_t s);
+cudaError_t launch_unpack(const Geo& g, const uint64_t* p0, const uint64_t* p1, int nplanes,
+                          uint8_t* out, cudaStream_t s);
+cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* a, const uint64_t* b, long long n, cudaStream_t s);
+
+}  // namespace kmc

@@ -1,0 +1,549 @@
+// kmc_kernels.cu -- sm_100a kernels of the fractional-step KMC hot path.
+//
+// substep_kernel: one window e^{D L^c} of eq.(exact).
+//   ONE LANE OWNS ONE COARSE CELL.  The cell and its one-site halo live in registers as
+//   64-bit bitboards (bit-packed cell-major layout, kmc_internal.h); per event the lane
+//     1. derives every slot class's member mask by bit-sliced neighbour counting
+//        (the class is the rate-table index of eq.(Arrhenius) P:963-968 / Table COrates),
+//     2. lambda = sum_c popc(mask_c) * rate_c   (eq.(totalrate), exact u64)
+//     3. draws Philox4x32-10(k, gid, window) and the exponential clock tau = -ln U / lambda
+//        (fdlibm log, IEEE RN ops only -- DESIGN.md §3), stops when t + tau >= D (R5),
+//     4. picks class c with prob popc*rate/lambda and a uniform member site of c
+//        (eq.(skeleton)) with popc-based rank selection, and
+//     5. applies the event as XORs on the planes (partner sites outside the cell go to
+//        the halo boards, written back once per window with atomicXor of the delta).
+//   No tensor cores: this is not a contraction.  See DESIGN.md §8 for why a lane (not a
+//   warp) owns a cell: the per-event chain is serial, so 32 independent cells per warp
+//   give 32x the issue efficiency of a warp-cooperative scan.
+// observables_kernel (a8): integer counts, order-free.
+// pack / unpack: uint8 site-major <-> bit-packed cell-major.
+#include "kmc_internal.h"
+
+#include <cstdint>
+
+namespace kmc {
+
+// ---------------------------------------------------------------------------------------------
+// L0 arithmetic: Philox4x32-10 and the fdlibm log sequence.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+// natural log on [2^-53, 1] (normal inputs only), fdlibm e_log.c operation order, every
+// operation an explicit round-to-nearest intrinsic so nvcc cannot contract to FMA.
+__device__ __forceinline__ double log_spec(double x) {
+    const double ln2_hi = 0x1.62e42feep-1, ln2_lo = 0x1.a39ef35793c76p-33;
+    const double Lg1 = 0x1.5555555555593p-1, Lg2 = 0x1.999999997fa04p-2, Lg3 = 0x1.2492494229359p-2;
+    const double Lg4 = 0x1.c71c51d8e78afp-3, Lg5 = 0x1.7466496cb03dep-3, Lg6 = 0x1.39a09d078c69fp-3;
+    const double Lg7 = 0x1.2f112df3e5244p-3;
+    int hx = __double2hiint(x);
+    const int lx = __double2loint(x);
+    int k = (hx >> 20) - 1023;
+    hx &= 0x000fffff;
+    int i = (hx + 0x95f64) & 0x100000;
+    const double xn = __hiloint2double(hx | (i ^ 0x3ff00000), lx);
+    k += (i >> 20);
+    const double f = __dsub_rn(xn, 1.0);
+    const double dk = (double)k;
+    if ((0x000fffff & (2 + hx)) < 3) {
+        if (f == 0.0) {
+            if (k == 0) return 0.0;
+            return __dadd_rn(__dmul_rn(dk, ln2_hi), __dmul_rn(dk, ln2_lo));
+        }
+        const double R = __dmul_rn(__dmul_rn(f, f), __dsub_rn(0.5, __dmul_rn(0.33333333333333333, f)));
+        if (k == 0) return __dsub_rn(f, R);
+        return __dsub_rn(__dmul_rn(dk, ln2_hi), __dsub_rn(__dsub_rn(R, __dmul_rn(dk, ln2_lo)), f));
+    }
+    const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+    const double z = __dmul_rn(s, s);
+    i = hx - 0x6147a;
+    const double w = __dmul_rn(z, z);
+    const int j = 0x6b851 - hx;
+    const double t1 = __dmul_rn(w, __dadd_rn(Lg2, __dmul_rn(w, __dadd_rn(Lg4, __dmul_rn(w, Lg6)))));
+    const double t2 = __dmul_rn(z, __dadd_rn(Lg1, __dmul_rn(w, __dadd_rn(Lg3, __dmul_rn(w, __dadd_rn(Lg5, __dmul_rn(w, Lg7)))))));
+    i |= j;
+    const double R = __dadd_rn(t2, t1);
+    if (i > 0) {
+        const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+        if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, __dmul_rn(s, __dadd_rn(hfsq, R))));
+        return __dsub_rn(__dmul_rn(dk, ln2_hi),
+                         __dsub_rn(__dsub_rn(hfsq, __dadd_rn(__dmul_rn(s, __dadd_rn(hfsq, R)), __dmul_rn(dk, ln2_lo))), f));
+    }
+    if (k == 0) return __dsub_rn(f, __dmul_rn(s, __dsub_rn(f, R)));
+    return __dsub_rn(__dmul_rn(dk, ln2_hi), __dsub_rn(__dsub_rn(__dmul_rn(s, __dsub_rn(f, R)), __dmul_rn(dk, ln2_lo)), f));
+}
+
+// position of the k-th (0-based) set bit of a 64-bit word (k < popc(m))
+__device__ __forceinline__ int select_bit64(uint64_t m, uint32_t k) {
+    uint32_t w = (uint32_t)m;
+    int pos = 0;
+    const uint32_t pl = __popc(w);
+    if (k >= pl) { k -= pl; w = (uint32_t)(m >> 32); pos = 32; }
+    uint32_t c = __popc(w & 0xFFFFu);
+    if (k >= c) { k -= c; w >>= 16; pos += 16; }
+    c = __popc(w & 0xFFu);
+    if (k >= c) { k -= c; w >>= 8; pos += 8; }
+    c = __popc(w & 0xFu);
+    if (k >= c) { k -= c; w >>= 4; pos += 4; }
+    c = __popc(w & 0x3u);
+    if (k >= c) { k -= c; w >>= 2; pos += 2; }
+    c = w & 1u;
+    if (k >= c) { pos += 1; }
+    return pos;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Models: class masks in canonical order and per-class XOR descriptors.
+// desc bits: 0 anchor toggles plane0, 1 anchor toggles plane1, 2 partner toggles plane0,
+//            3 partner toggles plane1, 4-5 direction, 6 has partner.
+// Directions d: 0 = -x, 1 = +x, 2 = -y, 3 = +y.
+// nb[p][d] = bitboard of plane p at the neighbour x+e_d of every cell site.
+// ---------------------------------------------------------------------------------------------
+constexpr int D_A0 = 1, D_A1 = 2, D_P0 = 4, D_P1 = 8, D_HASP = 64;
+__host__ __device__ constexpr int dsh(int d) { return d << 4; }
+
+// n == k masks from the z neighbour boards of plane 0 (bit-sliced adder)
+template <int NDIM>
+__device__ __forceinline__ void eq_counts(const uint64_t* nb, uint64_t* eq) {
+    if (NDIM == 1) {
+        eq[0] = ~(nb[0] | nb[1]);
+        eq[1] = nb[0] ^ nb[1];
+        eq[2] = nb[0] & nb[1];
+    } else {
+        const uint64_t s1 = nb[0] ^ nb[1], c1 = nb[0] & nb[1];
+        const uint64_t s2 = nb[2] ^ nb[3], c2 = nb[2] & nb[3];
+        const uint64_t b0 = s1 ^ s2, cr = s1 & s2;
+        const uint64_t b1 = c1 ^ c2 ^ cr;
+        const uint64_t b2 = (c1 & c2) | (cr & (c1 ^ c2));
+        eq[0] = ~(b0 | b1 | b2);
+        eq[1] = b0 & ~b1 & ~b2;
+        eq[2] = ~b0 & b1 & ~b2;
+        eq[3] = b0 & b1 & ~b2;
+        eq[4] = b2;                                       // n = 4 (b2 set implies b0 = b1 = 0)
+    }
+}
+
+template <int KIND, int NDIM> struct Model;
+
+template <int NDIM> struct Model<0, NDIM> {                    // ADSDES
+    static constexpr int Z = 2 * NDIM, NP = 1, NC = 2 + Z;
+    __device__ static int desc(int) { return D_A0; }
+    __device__ static void masks(const uint64_t* P, const uint64_t (*nb)[4], uint64_t valid, uint64_t* m) {
+        uint64_t eq[Z + 1];
+        eq_counts<NDIM>(nb[0], eq);
+        m[0] = valid & ~P[0];
+#pragma unroll
+        for (int n = 0; n <= Z; ++n) m[1 + n] = P[0] & eq[n];
+    }
+};
+
+template <int NDIM> struct Model<1, NDIM> {                    // ADSDES_DIFF
+    static constexpr int Z = 2 * NDIM, NP = 1, NC = 2 + Z + Z * Z;
+    __device__ static int desc(int c) {
+        if (c < 2 + Z) return D_A0;
+        const int d = (c - 2 - Z) / Z;
+        return D_A0 | D_P0 | D_HASP | dsh(d);
+    }
+    __device__ static void masks(const uint64_t* P, const uint64_t (*nb)[4], uint64_t valid, uint64_t* m) {
+        uint64_t eq[Z + 1];
+        eq_counts<NDIM>(nb[0], eq);
+        m[0] = valid & ~P[0];
+#pragma unroll
+        for (int n = 0; n <= Z; ++n) m[1 + n] = P[0] & eq[n];
+#pragma unroll
+        for (int d = 0; d < Z; ++d) {
+            const uint64_t mover = P[0] & ~nb[0][d];
+#pragma unroll
+            for (int n = 0; n < Z; ++n) m[2 + Z + d * Z + n] = mover & eq[n];
+        }
+    }
+};
+
+template <int KIND, int NDIM> struct ZgbModel {                // ZGB (KIND 2) / ZGB_DIFF (KIND 3)
+    static constexpr int Z = 2 * NDIM, NP = 2, NC = 1 + 3 * Z + (KIND == 3 ? Z : 0);
+    __device__ static int desc(int c) {
+        if (c == 0) return D_A0;                                   // CO adsorb
+        const int g = (c - 1) / Z, d = (c - 1) % Z;
+        if (g == 0) return D_A1 | D_P1 | D_HASP | dsh(d);          // O2 adsorb: x, y -> O
+        if (g == 1) return D_A0 | D_P1 | D_HASP | dsh(d);          // CO(x) + O(y) -> vacant
+        if (g == 2) return D_A1 | D_P0 | D_HASP | dsh(d);          // O(x) + CO(y) -> vacant
+        return D_A0 | D_P0 | D_HASP | dsh(d);                      // CO hop x -> y
+    }
+    __device__ static void masks(const uint64_t* P, const uint64_t (*nb)[4], uint64_t valid, uint64_t* m) {
+        const uint64_t vac = valid & ~(P[0] | P[1]);
+        m[0] = vac;
+#pragma unroll
+        for (int d = 0; d < Z; ++d) {
+            const uint64_t vnb = ~(nb[0][d] | nb[1][d]);
+            m[1 + d] = vac & vnb;
+            m[1 + Z + d] = P[0] & nb[1][d];
+            m[1 + 2 * Z + d] = P[1] & nb[0][d];
+            if (KIND == 3) m[1 + 3 * Z + d] = P[0] & vnb;
+        }
+    }
+};
+template <int NDIM> struct Model<2, NDIM> : ZgbModel<2, NDIM> {};
+template <int NDIM> struct Model<3, NDIM> : ZgbModel<3, NDIM> {};
+
+// ---------------------------------------------------------------------------------------------
+// The window kernel.
+// ---------------------------------------------------------------------------------------------
+template <int KIND, int NDIM>
+__global__ void __launch_bounds__(256)
+substep_kernel(const SubstepArgs a, const long long nactive) {
+    using M = Model<KIND, NDIM>;
+    constexpr int NP = M::NP, NC = M::NC, Z = M::Z;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const Geo& g = a.g;
+    unsigned k = 0;
+    if (t < nactive) {
+        // ---- which cell: active cells of colour c, R6 colouring on GLOBAL cell coordinates ----
+        const int half = g.Mx >> 1;
+        const int j = (int)(t % half);
+        const long long rest = t / half;
+        const int r = (int)(rest % g.R);
+        const int rowsel = (int)(rest / g.R);
+        int cy, cx;
+        if (NDIM == 1) {
+            cy = 0;
+            cx = 2 * j + a.colour;
+        } else if (a.C == 2) {
+            cy = rowsel;
+            cx = 2 * j + ((a.colour + g.row_offset + cy) & 1);
+        } else {
+            cy = 2 * rowsel + (a.colour >> 1);
+            cx = 2 * j + (a.colour & 1);
+        }
+        const int gy = g.row_offset + cy;
+        const unsigned long long gid =
+            (unsigned long long)(g.rep_offset + r) * (unsigned long long)g.M_global + (unsigned long long)gy * g.Mx + cx;
+        const long long rowlen = (long long)g.R * g.Mx;
+        const int sy = cy + g.ghost;
+        int syN = sy - 1, syS = sy + 1;
+        if (!g.ghost) {
+            if (syN < 0) syN += g.My_local;
+            if (syS >= g.My_local) syS -= g.My_local;
+        }
+        const int cxW = cx == 0 ? g.Mx - 1 : cx - 1;
+        const int cxE = cx == g.Mx - 1 ? 0 : cx + 1;
+        const long long base = (long long)sy * rowlen + (long long)r * g.Mx;
+        const long long iC = base + cx, iW = base + cxW, iE = base + cxE;
+        const long long iN = (long long)syN * rowlen + (long long)r * g.Mx + cx;
+        const long long iS = (long long)syS * rowlen + (long long)r * g.Mx + cx;
+        uint64_t* planes[2] = {a.plane0, a.plane1};
+
+        // ---- a3: stage the closure (cell + one-site halo) into registers ----
+        uint64_t P[NP], h[NP][4], h0[NP][4];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const uint64_t* pl = planes[p];
+            P[p] = pl[iC];
+            h[p][0] = (pl[iW] >> (g.qx - 1)) & g.col0;           // sigma(x-1) seen by column 0
+            h[p][1] = (pl[iE] << (g.qx - 1)) & g.colL;           // sigma(x+1) seen by column qx-1
+            if (NDIM == 2) {
+                h[p][2] = (pl[iN] >> g.shN) & g.row0;             // sigma(y-1) seen by row 0
+                h[p][3] = (pl[iS] << g.shN) & g.rowL;             // sigma(y+1) seen by row qy-1
+            } else {
+                h[p][2] = h[p][3] = 0;
+            }
+#pragma unroll
+            for (int d = 0; d < 4; ++d) h0[p][d] = h[p][d];
+        }
+        const uint64_t notcol0 = g.valid & ~g.col0, notcolL = g.valid & ~g.colL;
+        const uint64_t notrow0 = g.valid & ~g.row0, notrowL = g.valid & ~g.rowL;
+        const uint32_t w_lo = a.w_lo, w_hi = a.w_hi_tag, gid32 = (uint32_t)gid;
+        double tclock = 0.0;
+
+        // ---- a5: the per-cell SSA event loop ----
+        for (;;) {
+            uint64_t nb[NP][4];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                nb[p][0] = ((P[p] << 1) & notcol0) | h[p][0];
+                nb[p][1] = ((P[p] >> 1) & notcolL) | h[p][1];
+                if (NDIM == 2) {
+                    nb[p][2] = ((P[p] << g.qx) & g.valid) | h[p][2];
+                    nb[p][3] = (P[p] >> g.qx) | h[p][3];
+                } else {
+                    nb[p][2] = nb[p][3] = 0;
+                }
+            }
+            uint64_t m[NC];
+            M::masks(P, nb, g.valid, m);
+            uint32_t cnt[NC];
+            uint64_t lam = 0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                cnt[c] = __popcll(m[c]);
+                lam += (uint64_t)cnt[c] * a.rate[c];
+            }
+            if (lam == 0) break;                                   // quiescent cell
+            const uint4 x = philox4x32_10(make_uint4(k, gid32, w_lo, w_hi), a.key0, a.key1);
+            const uint64_t j53 = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
+            const double U = __dmul_rn(__ull2double_rn(j53 + 1ull), 0x1p-53);
+            const double E = -log_spec(U);
+            const double lamd = __dmul_rn(__ull2double_rn(lam), a.inv_scale);
+            const double tau = __ddiv_rn(E, lamd);
+            const double tn = __dadd_rn(tclock, tau);
+            if (tn >= a.D) break;                                  // R5: pending event discarded
+            tclock = tn;
+            // class: smallest c with prefix(c) > r, r = floor(x2 * lambda / 2^32)
+            const uint64_t rr = (uint64_t)x.z * (lam >> 32) + (uint64_t)__umulhi(x.z, (uint32_t)lam);
+            uint64_t cum = 0, selm = m[NC - 1];
+            uint32_t selc = cnt[NC - 1];
+            int seld = M::desc(NC - 1);
+            bool found = false;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                cum += (uint64_t)cnt[c] * a.rate[c];
+                const bool hit = !found && cum > rr;
+                if (hit) { selm = m[c]; selc = cnt[c]; seld = M::desc(c); }
+                found = found || hit;
+            }
+            // site: the kk-th member of the class in row-major order, kk = floor(x3 * cnt / 2^32)
+            const uint32_t kk = __umulhi(x.w, selc);
+            const int s = select_bit64(selm, kk);
+            const uint64_t ab = 1ull << s;
+            if (seld & D_A0) P[0] ^= ab;
+            if (NP > 1 && (seld & D_A1)) P[NP - 1] ^= ab;
+            if (seld & D_HASP) {
+                const int d = (seld >> 4) & 3;
+                uint64_t inner, pb;
+                if (d == 0)      { inner = notcol0; pb = ab >> 1; }
+                else if (d == 1) { inner = notcolL; pb = ab << 1; }
+                else if (d == 2) { inner = notrow0; pb = ab >> g.qx; }
+                else             { inner = notrowL; pb = ab << g.qx; }
+                const bool in_cell = (ab & inner) != 0;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    if (seld & (D_P0 << p)) {
+                        if (in_cell) P[p] ^= pb;
+                        else {
+#pragma unroll
+                            for (int dd = 0; dd < 4; ++dd)
+                                if (dd == d) h[p][dd] ^= ab;
+                        }
+                    }
+                }
+            }
+            ++k;
+        }
+
+        // ---- a6: write back once per window ----
+        if (k) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                uint64_t* pl = planes[p];
+                pl[iC] = P[p];
+                if (KIND != 0) {   // halo deltas (pair / hop events): disjoint bits, order-free XOR
+                    const uint64_t dW = h[p][0] ^ h0[p][0], dE = h[p][1] ^ h0[p][1];
+                    if (dW) atomicXor((unsigned long long*)&pl[iW], (unsigned long long)(dW << (g.qx - 1)));
+                    if (dE) atomicXor((unsigned long long*)&pl[iE], (unsigned long long)(dE >> (g.qx - 1)));
+                    if (NDIM == 2) {
+                        const uint64_t dN = h[p][2] ^ h0[p][2], dS = h[p][3] ^ h0[p][3];
+                        if (dN) atomicXor((unsigned long long*)&pl[iN], (unsigned long long)(dN << g.shN));
+                        if (dS) atomicXor((unsigned long long*)&pl[iS], (unsigned long long)(dS >> g.shN));
+                    }
+                }
+            }
+            a.wev[(long long)cy * rowlen + (long long)r * g.Mx + cx] += k;
+        }
+    }
+    // event total: warp-aggregated
+    unsigned long long kw = k;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kw += __shfl_xor_sync(0xffffffffu, kw, o);
+    if ((threadIdx.x & 31) == 0 && kw) atomicAdd(a.ev_total, kw);
+}
+
+template <int KIND, int NDIM>
+static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
+    if (nactive <= 0) return cudaSuccess;
+    const int bs = 256;
+    const long long nb = (nactive + bs - 1) / bs;
+    substep_kernel<KIND, NDIM><<<(unsigned)nb, bs, 0, s>>>(a, nactive);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cudaStream_t s) {
+    const bool two = a.g.ndim == 2;
+    switch (kind) {
+    case 0: return two ? launch_t<0, 2>(a, nactive, s) : launch_t<0, 1>(a, nactive, s);
+    case 1: return two ? launch_t<1, 2>(a, nactive, s) : launch_t<1, 1>(a, nactive, s);
+    case 2: return two ? launch_t<2, 2>(a, nactive, s) : launch_t<2, 1>(a, nactive, s);
+    case 3: return two ? launch_t<3, 2>(a, nactive, s) : launch_t<3, 1>(a, nactive, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a8: observables.  Counters (u64): [0..3] n_state, [4..19] by colour [c*4+s],
+// [20..35] ordered nearest-neighbour bonds (x, x+e) for e in {+x, +y}: [20 + a*4 + b].
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
+    const Geo& g = a.g;
+    __shared__ unsigned long long sh[kObsCounters];
+    for (int i = threadIdx.x; i < kObsCounters; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    uint32_t acc[kObsCounters];
+#pragma unroll
+    for (int i = 0; i < kObsCounters; ++i) acc[i] = 0;
+    const long long rowlen = (long long)g.R * g.Mx;
+    const long long ncell = (long long)g.My_local * rowlen;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int cx = (int)(t % g.Mx);
+        const long long rest = t / g.Mx;
+        const int r = (int)(rest % g.R);
+        const int cy = (int)(rest / g.R);
+        const int sy = cy + g.ghost;
+        int syS = sy + 1;
+        if (!g.ghost && syS >= g.My_local) syS -= g.My_local;
+        const int cxE = cx == g.Mx - 1 ? 0 : cx + 1;
+        const long long iC = (long long)sy * rowlen + (long long)r * g.Mx + cx;
+        const long long iE = (long long)sy * rowlen + (long long)r * g.Mx + cxE;
+        const long long iS = (long long)syS * rowlen + (long long)r * g.Mx + cx;
+        uint64_t A[3], Bx[3], By[3];
+        const uint64_t notcolL = g.valid & ~g.colL;
+        uint64_t occ = 0, occx = 0, occy = 0;
+        for (int p = 0; p < a.nplanes; ++p) {
+            const uint64_t* pl = p == 0 ? a.plane0 : a.plane1;
+            const uint64_t P = pl[iC];
+            A[1 + p] = P;
+            Bx[1 + p] = ((P >> 1) & notcolL) | ((pl[iE] << (g.qx - 1)) & g.colL);
+            By[1 + p] = (g.ndim == 2) ? ((P >> g.qx) | ((pl[iS] << g.shN) & g.rowL)) : 0;
+            occ |= A[1 + p]; occx |= Bx[1 + p]; occy |= By[1 + p];
+        }
+        A[0] = g.valid & ~occ;
+        Bx[0] = g.valid & ~occx;
+        By[0] = g.valid & ~occy;
+        const int ns = a.nplanes + 1;
+        const int gy = g.row_offset + cy;
+        int colour;
+        if (a.C == 2) colour = g.ndim == 1 ? (cx & 1) : ((cx + gy) & 1);
+        else colour = (cx & 1) + 2 * (gy & 1);
+        for (int s = 0; s < ns; ++s) {
+            const uint32_t c = __popcll(A[s]);
+            acc[s] += c;
+            acc[4 + colour * 4 + s] += c;
+            for (int b = 0; b < ns; ++b) {
+                acc[20 + s * 4 + b] += __popcll(A[s] & Bx[b]);
+                if (g.ndim == 2) acc[20 + s * 4 + b] += __popcll(A[s] & By[b]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kObsCounters; ++i) {
+        const uint32_t v = __reduce_add_sync(0xffffffffu, acc[i]);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sh[i], (unsigned long long)v);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kObsCounters; i += blockDim.x)
+        if (sh[i]) atomicAdd(&a.out[i], sh[i]);
+}
+
+cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long ncell = (long long)a.g.My_local * a.g.R * a.g.Mx;
+    long long nb = (ncell + 255) / 256;
+    if (nb > 4LL * nsm) nb = 4LL * nsm;
+    if (nb < 1) nb = 1;
+    observables_kernel<<<(unsigned)nb, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// pack / unpack between uint8 site-major [R][H_local][W] and the bit-packed planes.
+// ---------------------------------------------------------------------------------------------
+__global__ void pack_kernel(const Geo g, const uint8_t* __restrict__ in, uint64_t* p0, uint64_t* p1,
+                            int nstates, unsigned int* err) {
+    const long long ncell = (long long)g.My_local * g.R * g.Mx;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncell) return;
+    const int cx = (int)(t % g.Mx);
+    const long long rest = t / g.Mx;
+    const int r = (int)(rest % g.R);
+    const int cy = (int)(rest / g.R);
+    const long long W = (long long)g.Mx * g.qx;
+    const long long H = (long long)g.My_local * g.qy;
+    uint64_t a = 0, b = 0;
+    unsigned bad = 0;
+    for (int ly = 0; ly < g.qy; ++ly) {
+        const uint8_t* row = in + ((long long)r * H + (long long)cy * g.qy + ly) * W + (long long)cx * g.qx;
+        for (int lx = 0; lx < g.qx; ++lx) {
+            const unsigned v = row[lx];
+            const int s = ly * g.qx + lx;
+            if (v >= (unsigned)nstates) { bad = 1; continue; }
+            a |= (uint64_t)(v == 1) << s;
+            b |= (uint64_t)(v == 2) << s;
+        }
+    }
+    const long long idx = ((long long)(cy + g.ghost) * g.R + r) * g.Mx + cx;
+    p0[idx] = a;
+    if (p1) p1[idx] = b;
+    if (bad) atomicOr(err, 1u);
+}
+
+__global__ void unpack_kernel(const Geo g, const uint64_t* __restrict__ p0, const uint64_t* __restrict__ p1,
+                              int nplanes, uint8_t* __restrict__ out) {
+    const long long ncell = (long long)g.My_local * g.R * g.Mx;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncell) return;
+    const int cx = (int)(t % g.Mx);
+    const long long rest = t / g.Mx;
+    const int r = (int)(rest % g.R);
+    const int cy = (int)(rest / g.R);
+    const long long W = (long long)g.Mx * g.qx;
+    const long long H = (long long)g.My_local * g.qy;
+    const long long idx = ((long long)(cy + g.ghost) * g.R + r) * g.Mx + cx;
+    const uint64_t a = p0[idx];
+    const uint64_t b = nplanes > 1 ? p1[idx] : 0;
+    for (int ly = 0; ly < g.qy; ++ly) {
+        uint8_t* row = out + ((long long)r * H + (long long)cy * g.qy + ly) * W + (long long)cx * g.qx;
+        for (int lx = 0; lx < g.qx; ++lx) {
+            const int s = ly * g.qx + lx;
+            row[lx] = (uint8_t)(((a >> s) & 1) | (((b >> s) & 1) << 1));
+        }
+    }
+}
+
+cudaError_t launch_pack(const Geo& g, const uint8_t* in, uint64_t* p0, uint64_t* p1, int nstates,
+                        unsigned int* err, cudaStream_t s) {
+    const long long ncell = (long long)g.My_local * g.R * g.Mx;
+    if (ncell == 0) return cudaSuccess;
+    pack_kernel<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(g, in, p0, p1, nstates, err);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const Geo& g, const uint64_t* p0, const uint64_t* p1, int nplanes,
+                          uint8_t* out, cudaStream_t s) {
+    const long long ncell = (long long)g.My_local * g.R * g.Mx;
+    if (ncell == 0) return cudaSuccess;
+    unpack_kernel<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(g, p0, p1, nplanes, out);
+    return cudaGetLastError();
+}
+
+__global__ void xor_into_kernel(uint64_t* dst, const uint64_t* src, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] ^= src[i];
+}
+
+cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* src, const uint64_t* /*unused*/, long long n,
+                            cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    xor_into_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dst, src, n);
+    return cudaGetLastError();
+}
+
+}  // namespace kmc

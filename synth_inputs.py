@@ -9,16 +9,28 @@ import numpy as np
 SEED_BASE = 0x5EED0001
 
 
-def bernoulli_lattice(shape, p=0.5, seed=SEED_BASE):
-    """Sites occupied (state 1) independently with probability p; uint8 site-major."""
+def bernoulli_lattice(shape, p=0.5, seed=SEED_BASE, chunk=1 << 24):
+    """Sites occupied (state 1) independently with probability p; uint8 site-major.
+    Drawn in chunks of `chunk` sites (float32 uniforms) so 32768^2 lattices fit in memory."""
     rng = np.random.default_rng(seed)
-    return (rng.random(shape) < p).astype(np.uint8)
+    out = np.empty(int(np.prod(shape)), dtype=np.uint8)
+    p32 = np.float32(p)
+    for i in range(0, out.size, chunk):
+        n = min(chunk, out.size - i)
+        out[i:i + n] = rng.random(n, dtype=np.float32) < p32
+    return out.reshape(shape)
 
 
 def categorical_lattice(shape, probs, seed=SEED_BASE):
     """Sites in state s with probability probs[s] (ZGB: 0 vacant, 1 CO, 2 O)."""
     rng = np.random.default_rng(seed)
-    return rng.choice(len(probs), size=shape, p=probs).astype(np.uint8)
+    cum = np.cumsum(np.asarray(probs, dtype=np.float64))[:-1].astype(np.float32)
+    out = np.empty(int(np.prod(shape)), dtype=np.uint8)
+    chunk = 1 << 24
+    for i in range(0, out.size, chunk):
+        n = min(chunk, out.size - i)
+        out[i:i + n] = np.searchsorted(cum, rng.random(n, dtype=np.float32), side="right")
+    return out.reshape(shape)
 
 
 def colour_full_lattice(shape, ndim, cell, C, colour=1):

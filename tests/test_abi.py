@@ -1,0 +1,69 @@
+"""The C-ABI library loads and exports every symbol include/kmc.h declares; host-side
+validation and the partition plan (no GPU needed)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1105_4673_b200 as kmc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "kmc.h")).read()
+    return sorted(set(re.findall(r"\b(kmc_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = kmc.lib()
+    declared = header_symbols()
+    assert declared == sorted(kmc.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", kmc.LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared:
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", kmc.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version():
+    assert b"sm_100a" in kmc.lib().kmc_version()
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(ndim=2, dims=(64, 60), cell=(8, 8)), kmc.KMC_EPARTITION),          # not divisible
+    (dict(ndim=2, dims=(72, 64), cell=(8, 8)), kmc.KMC_EPARTITION),          # 9 cell rows (odd)
+    (dict(ndim=2, dims=(64, 64), cell=(16, 8)), kmc.KMC_EPARTITION),         # 128 sites > 64
+    (dict(ndim=2, dims=(64, 64), cell=(8, 8), kind="adsdes_diff", colours=2), kmc.KMC_EPARTITION),  # R6
+    (dict(ndim=1, dims=(64,), cell=(1,), kind="zgb"), kmc.KMC_EPARTITION),    # R7 extent < 2
+    (dict(ndim=1, dims=(64,), cell=(8,), colours=4), kmc.KMC_EPARTITION),
+    (dict(ndim=3, dims=(64,), cell=(8,)), kmc.KMC_EINVAL),
+    (dict(ndim=2, dims=(64, 64), cell=(8, 8), ca=-1.0), kmc.KMC_EINVAL),      # negative rate
+])
+def test_create_validation_before_any_device_work(kw, status):
+    with pytest.raises(kmc.KmcError) as e:
+        kmc.KMC(**kw)
+    assert e.value.status == status
+
+
+def test_partition_plan_slabs_and_ring():
+    plans = [kmc.partition_plan(2, (256, 64), (8, 8), 1, "adsdes", 4, r) for r in range(4)]
+    assert [p["row_offset"] for p in plans] == [0, 8, 16, 24]
+    assert all(p["rows_local"] == 8 for p in plans)
+    assert [p["rank_up"] for p in plans] == [3, 0, 1, 2]
+    assert [p["rank_down"] for p in plans] == [1, 2, 3, 0]
+    # 1D: replicas are split, no exchange
+    p = kmc.partition_plan(1, (1024,), (32,), 8, "adsdes", 4, 3)
+    assert (p["replica_offset"], p["replicas_local"], p["rank_up"]) == (6, 2, -1)
+    with pytest.raises(kmc.KmcError):
+        kmc.partition_plan(2, (256, 64), (8, 8), 1, "adsdes", 3, 0)    # 32 cell rows / 3 ranks
+    with pytest.raises(kmc.KmcError):
+        kmc.partition_plan(2, (64, 64), (8, 8), 1, "adsdes", 8, 0)     # 1 cell row per rank (< 2)

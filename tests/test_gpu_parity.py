@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the O2 oracle, bit-exact after
+EVERY window (lattice, per-cell event counts, totals) and on the observables.
+
+Bar: integer / bit work is bit-exact.  The clock is FP64 but both sides
+execute the same IEEE operation sequence, so the lattice is bit-exact too.
+"""
+import numpy as np
+import pytest
+
+import synth_inputs as si
+from oracle.fskmc import FSKMC, model_params
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def make_pair(ndim, dims, cell, kind, params, colours=0, replicas=1, seed=1234):
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    gpu = kmc.KMC(ndim, dims, cell, kind=kind, colours=colours, replicas=replicas, seed=seed, **params)
+    orc = FSKMC(ndim, dims, cell, kind, model_params(**params), colours=colours, replicas=replicas, seed=seed)
+    return gpu, orc
+
+
+def assert_same_state(gpu, orc, tag=""):
+    a = gpu.get_config()
+    b = orc.get_config()
+    if not np.array_equal(a, b):
+        diff = np.argwhere(a != b)
+        raise AssertionError(f"{tag}: {len(diff)} sites differ, first {diff[:4].tolist()}")
+    obs = gpu.observables(per_cell=True)
+    assert obs["events"] == orc.events, (tag, obs["events"], orc.events)
+    R, My, Mx = obs["per_cell_events"].shape
+    assert np.array_equal(obs["per_cell_events"].reshape(-1), orc.W_events), tag
+    assert obs["windows"] == orc.window
+
+
+def run_windows(gpu, orc, scheme, dt, nmacro):
+    """Drive both through the same schedule one window at a time (oracle schedule), and
+    separately check the library's own kmc_run schedule reproduces it."""
+    from oracle.fskmc import substeps, SCHEME
+    sc = SCHEME[scheme]
+    for i in range(nmacro):
+        for colour, D in substeps(sc, orc.C, dt, orc.seed, orc.window):
+            gpu.substep(colour, D)
+            orc.substep(colour, D)
+            assert_same_state(gpu, orc, f"macro {i} colour {colour}")
+        orc.time += dt
+
+
+CASES = {
+    # name: (ndim, dims, cell, kind, params, colours, replicas, init, scheme, dt, nmacro)
+    "1d_noninteracting_cfg1": (1, (1024,), (32,), "adsdes", dict(ca=1.0, cd=0.5, beta=1.0, K=0.0, h=0.0), 0, 16, 0.0, "lie", 0.5, 3),
+    "1d_ising_strang": (1, (4096,), (32,), "adsdes", dict(ca=1, cd=1, beta=2.0, K=1.0, h=-0.5), 0, 3, 0.5, "strang", 0.5, 3),
+    "1d_ising_q4_random": (1, (512,), (4,), "adsdes", dict(ca=1, cd=1, beta=1.0, K=1.0, h=-1.0), 0, 4, 0.5, "random", 1.0, 3),
+    "1d_ising_q64": (1, (1024,), (64,), "adsdes", dict(ca=1, cd=1, beta=1.0, K=1.0, h=-1.0), 0, 2, 0.3, "lie", 1.0, 2),
+    "2d_ising_8x8": (2, (128, 128), (8, 8), "adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), 0, 1, 0.5, "lie", 1.0, 2),
+    "2d_ising_random": (2, (64, 64), (8, 8), "adsdes", dict(ca=1, cd=1, beta=2.2, K=1.0, h=-2.0), 0, 2, 0.9, "random", 1.0, 2),
+    "2d_ising_rect_cell": (2, (64, 128), (2, 16), "adsdes", dict(ca=1, cd=1, beta=1.0, K=1.0, h=-2.0), 0, 1, 0.5, "strang", 0.5, 2),
+    "2d_ising_1x1_cell": (2, (16, 16), (1, 1), "adsdes", dict(ca=1, cd=1, beta=1.0, K=1.0, h=-2.0), 0, 3, 0.5, "lie", 0.7, 3),
+    "2d_ising_ragged": (2, (24, 40), (4, 4), "adsdes", dict(ca=0.7, cd=1.3, beta=1.2, K=0.8, h=-1.0), 0, 5, 0.4, "strang", 1.0, 2),
+    "2d_diffusion_4col": (2, (64, 64), (8, 8), "adsdes_diff", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0, c_hop=1.0), 0, 1, 0.5, "strang", 0.5, 2),
+    "2d_diffusion_q2": (2, (32, 32), (2, 2), "adsdes_diff", dict(ca=0.3, cd=0.3, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), 0, 2, 0.5, "lie", 0.5, 2),
+    "1d_diffusion": (1, (512,), (8,), "adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-1.0, c_hop=1.5), 0, 3, 0.5, "lie", 0.5, 3),
+    "2d_zgb": (2, (64, 64), (4, 4), "zgb", dict(k1=0.4, k2=1.0), 0, 1, None, "lie", 0.5, 3),
+    "2d_zgb_diff": (2, (32, 64), (4, 8), "zgb_diff", dict(k1=0.45, k2=1.0, c_hop=1.0), 0, 2, None, "strang", 0.5, 2),
+    "1d_zgb": (1, (256,), (4,), "zgb", dict(k1=0.4, k2=1.0), 0, 4, None, "random", 0.5, 3),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_bit_exact_every_window(name):
+    ndim, dims, cell, kind, params, C, R, init, scheme, dt, nmacro = CASES[name]
+    gpu, orc = make_pair(ndim, dims, cell, kind, params, C, R)
+    shape = gpu.local_shape
+    if init is None:
+        lat = si.categorical_lattice(shape, [0.6, 0.2, 0.2], seed=si.SEED_BASE + 5)
+    else:
+        lat = si.bernoulli_lattice(shape, init, seed=si.SEED_BASE + 3)
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    assert_same_state(gpu, orc, "init")
+    run_windows(gpu, orc, scheme, dt, nmacro)
+    assert orc.events > 0
+
+
+@pytest.mark.parametrize("scheme", ["lie", "strang", "random"])
+def test_library_schedule_matches_oracle_run(scheme):
+    """kmc_run's own schedule (R1-R4, R20 truncation) equals the oracle's run()."""
+    p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)
+    gpu, orc = make_pair(2, (64, 64), (8, 8), "adsdes", p, 0, 2)
+    lat = si.bernoulli_lattice(gpu.local_shape, 0.5, seed=7)
+    gpu.set_config(lat); orc.set_config(lat)
+    tr_g = gpu.run(2.5, 1.0, scheme)
+    tr_o = orc.run(2.5, 1.0, scheme)
+    assert tr_g and tr_o
+    assert_same_state(gpu, orc, scheme)
+    assert abs(gpu.get_state()[1] - 2.5) < 1e-12
+
+
+def test_observables_match_oracle():
+    for kind, params, init in [("adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), 0.5),
+                               ("zgb", dict(k1=0.4, k2=1.0), None)]:
+        gpu, orc = make_pair(2, (64, 96), (4, 8), kind, params, 0, 2)
+        lat = (si.bernoulli_lattice(gpu.local_shape, 0.4, seed=3) if init is not None
+               else si.categorical_lattice(gpu.local_shape, [0.5, 0.3, 0.2], seed=3))
+        gpu.set_config(lat); orc.set_config(lat)
+        gpu.run(1.0, 0.5, "lie"); orc.run(1.0, 0.5, "lie")
+        a, b = gpu.observables(), orc.observables()
+        for key in ("n_state", "nn_pairs", "n_state_by_colour"):
+            assert np.array_equal(a[key], b[key]), (kind, key, a[key], b[key])
+        assert a["events"] == b["events"] and a["windows"] == b["windows"]
+        assert np.allclose(a["coverage"], b["coverage"], rtol=0, atol=1e-15)
+        assert abs(a["energy"] - b["energy"]) <= 1e-9 * max(1.0, abs(b["energy"]))
+
+
+def test_resume_run_split_equals_whole():
+    p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0, c_hop=1.0)
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    lat = si.bernoulli_lattice((1, 64, 64), 0.5, seed=9)
+    a = kmc.KMC(2, (64, 64), (8, 8), kind="adsdes_diff", seed=5, **p)
+    b = kmc.KMC(2, (64, 64), (8, 8), kind="adsdes_diff", seed=5, **p)
+    a.set_config(lat); b.set_config(lat)
+    a.run(3.0, 1.0, "strang")
+    b.run(1.0, 1.0, "strang"); b.run(2.0, 1.0, "strang")
+    assert np.array_equal(a.get_config(), b.get_config())
+    # checkpoint / restore into a fresh context
+    w, t = a.get_state()
+    c = kmc.KMC(2, (64, 64), (8, 8), kind="adsdes_diff", seed=5, **p)
+    c.set_config(a.get_config()); c.set_state(w, t)
+    a.run(1.0, 1.0, "strang"); c.run(1.0, 1.0, "strang")
+    assert np.array_equal(a.get_config(), c.get_config())
+
+
+def test_degenerate_cases():
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    # all rates zero: quiescent cells, no events
+    g = kmc.KMC(2, (32, 32), (8, 8), kind="adsdes", ca=0.0, cd=0.0)
+    g.set_config(si.bernoulli_lattice(g.local_shape, 0.5, seed=1))
+    before = g.get_config()
+    g.run(5.0, 1.0, "lie")
+    assert np.array_equal(before, g.get_config()) and g.observables()["events"] == 0
+    # zero-duration window
+    g = kmc.KMC(2, (32, 32), (8, 8), kind="adsdes", ca=1.0, cd=1.0)
+    g.substep(0, 0.0)
+    assert g.observables()["events"] == 0
+    # invalid spin value: rejected, lattice unchanged
+    lat = si.bernoulli_lattice(g.local_shape, 0.5, seed=2)
+    g.set_config(lat)
+    bad = lat.copy(); bad[0, 3, 3] = 2
+    with pytest.raises(kmc.KmcError) as e:
+        g.set_config(bad)
+    assert e.value.status == kmc.KMC_EINVAL
+    assert np.array_equal(g.get_config(), lat)
+    with pytest.raises(kmc.KmcError):
+        g.substep(2, 1.0)          # colour out of range
+
+
+def test_device_buffers_roundtrip():
+    torch = _cuda()
+    import paper_1105_4673_b200 as kmc
+    g = kmc.KMC(2, (64, 64), (8, 8), kind="zgb", stream=torch.cuda.current_stream().cuda_stream)
+    lat = si.categorical_lattice(g.local_shape, [0.4, 0.3, 0.3], seed=4)
+    t = torch.from_numpy(lat).cuda()
+    g.set_config_device(t.data_ptr(), t.numel())
+    out = torch.empty_like(t)
+    g.get_config_device(out.data_ptr(), out.numel())
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), lat)
+    assert np.array_equal(g.get_config(), lat)
+
+
+@pytest.mark.parametrize("kind", ["adsdes", "zgb"])
+def test_full_size_sampled_cells(kind):
+    """BASELINE target size 32768^2 in the launch configuration bench.py times: one window on
+    the GPU; 512 sampled active cells recomputed by the oracle from the pre-window lattice
+    (cells of one colour are independent within a window, eq.(exact))."""
+    torch = _cuda()
+    import paper_1105_4673_b200 as kmc
+    wl = dict(si.WORKLOADS["ising2d_32768" if kind == "adsdes" else "zgb2d_32768"])
+    H, W = wl["dims"]
+    qy, qx = wl["cell"]
+    g = kmc.KMC(2, (H, W), (qy, qx), kind=kind, seed=99, **wl["params"])
+    if kind == "adsdes":
+        lat = si.bernoulli_lattice((1, H, W), 0.5, seed=si.SEED_BASE)
+    else:
+        lat = si.categorical_lattice((1, H, W), [0.5, 0.25, 0.25], seed=si.SEED_BASE)
+    g.set_config(lat)
+    g.run(2.0 * wl["dt"], wl["dt"], "lie")       # advance a little so the state is not the input
+    pre = g.get_config()
+    w0, _ = g.get_state()
+    ev_pre = g.observables(per_cell=True)["per_cell_events"][0]
+    colour = 1
+    D = wl["dt"]
+    g.substep(colour, D)
+    post = g.get_config()
+    ev_post = g.observables(per_cell=True)["per_cell_events"][0]
+    orc = FSKMC(2, (H, W), (qy, qx), kind, model_params(**wl["params"]), seed=99)
+    orc.set_config(pre)
+    rng = np.random.default_rng(17)
+    Mx, My = W // qx, H // qy
+    C = orc.C
+    cells = []
+    while len(cells) < 512:
+        cy, cx = int(rng.integers(My)), int(rng.integers(Mx))
+        col = ((cx + cy) & 1) if C == 2 else ((cx & 1) + 2 * (cy & 1))
+        if col == colour:
+            cells.append((0, cy, cx))
+    cells = np.array(sorted(set(cells)))
+    ev = orc.window_cells(cells, D, w0)
+    got = orc.get_config()
+    for (r, cy, cx), k in zip(cells, ev):
+        ys, xs = slice(cy * qy, (cy + 1) * qy), slice(cx * qx, (cx + 1) * qx)
+        assert np.array_equal(post[0, ys, xs], got[0, ys, xs]), (cy, cx)
+        assert int(ev_post[cy, cx]) - int(ev_pre[cy, cx]) == int(k), (cy, cx)
+    assert ev.sum() > 0
