@@ -131,7 +131,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kmc", choices=["kmc", "reference"])
     ap.add_argument("--workload", default="ising2d_32768", choices=sorted(si.WORKLOADS))
@@ -197,6 +197,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
+    time.sleep(0.6)                                   # let nvidia-smi attach before the timed region
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)

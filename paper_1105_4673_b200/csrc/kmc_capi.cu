@@ -285,6 +285,10 @@ kmc_status do_substep(kmc_ctx* c, int colour, double D) {
     a.inv_scale = std::ldexp(1.0, -c->F);
     a.key0 = (uint32_t)c->geom.seed;
     a.key1 = (uint32_t)(c->geom.seed >> 32);
+    for (int i = 0; i < 10; ++i) {
+        a.rk0[i] = a.key0 + (uint32_t)i * 0x9E3779B9u;
+        a.rk1[i] = a.key1 + (uint32_t)i * 0xBB67AE85u;
+    }
     a.w_lo = (uint32_t)c->window;
     a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
     for (int i = 0; i < c->nclass; ++i) a.rate[i] = c->crate_u64[i];

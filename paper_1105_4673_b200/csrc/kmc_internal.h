@@ -40,6 +40,7 @@ struct SubstepArgs {
     double D;                        // window duration
     double inv_scale;                // 2^-F
     uint32_t key0, key1;             // Philox key = seed
+    uint32_t rk0[10], rk1[10];       // Philox round keys k + i*(W0, W1), i = 0..9 (warp-uniform)
     uint32_t w_lo, w_hi_tag;         // window id (tag EVT = 0 in bits 28..31)
     uint64_t rate[kMaxClass];        // u64 fixed-point class rates (R18)
 };

@@ -20,6 +20,7 @@
 #include "kmc_internal.h"
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace kmc {
 
@@ -196,75 +197,155 @@ template <int NDIM> struct Model<3, NDIM> : ZgbModel<3, NDIM> {};
 
 // ---------------------------------------------------------------------------------------------
 // The window kernel.
+//
+// Work distribution: the active cells of the colour are numbered 0..nactive-1 (row-major over
+// (row, replica, column pair)); warp w owns the contiguous chunk [w*chunk, (w+1)*chunk).  Each
+// lane runs one cell at a time; when its cell's window ends (clock past D or lambda = 0) the lane
+// writes the cell back and takes the next unclaimed cell of the warp's chunk (ballot + popc, no
+// atomics).  This keeps the 32 lanes busy although cells execute Poisson-distributed numbers of
+// events -- with one static cell per lane a warp would run max-over-lanes iterations.
 // ---------------------------------------------------------------------------------------------
-template <int KIND, int NDIM>
-__global__ void __launch_bounds__(256)
-substep_kernel(const SubstepArgs a, const long long nactive) {
-    using M = Model<KIND, NDIM>;
-    constexpr int NP = M::NP, NC = M::NC, Z = M::Z;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const Geo& g = a.g;
-    unsigned k = 0;
-    if (t < nactive) {
-        // ---- which cell: active cells of colour c, R6 colouring on GLOBAL cell coordinates ----
-        const int half = g.Mx >> 1;
-        const int j = (int)(t % half);
-        const long long rest = t / half;
-        const int r = (int)(rest % g.R);
-        const int rowsel = (int)(rest / g.R);
-        int cy, cx;
-        if (NDIM == 1) {
-            cy = 0;
-            cx = 2 * j + a.colour;
-        } else if (a.C == 2) {
-            cy = rowsel;
-            cx = 2 * j + ((a.colour + g.row_offset + cy) & 1);
-        } else {
-            cy = 2 * rowsel + (a.colour >> 1);
-            cx = 2 * j + (a.colour & 1);
-        }
-        const int gy = g.row_offset + cy;
-        const unsigned long long gid =
-            (unsigned long long)(g.rep_offset + r) * (unsigned long long)g.M_global + (unsigned long long)gy * g.Mx + cx;
-        const long long rowlen = (long long)g.R * g.Mx;
-        const int sy = cy + g.ghost;
-        int syN = sy - 1, syS = sy + 1;
-        if (!g.ghost) {
-            if (syN < 0) syN += g.My_local;
-            if (syS >= g.My_local) syS -= g.My_local;
-        }
-        const int cxW = cx == 0 ? g.Mx - 1 : cx - 1;
-        const int cxE = cx == g.Mx - 1 ? 0 : cx + 1;
-        const long long base = (long long)sy * rowlen + (long long)r * g.Mx;
-        const long long iC = base + cx, iW = base + cxW, iE = base + cxE;
-        const long long iN = (long long)syN * rowlen + (long long)r * g.Mx + cx;
-        const long long iS = (long long)syS * rowlen + (long long)r * g.Mx + cx;
-        uint64_t* planes[2] = {a.plane0, a.plane1};
+struct CellLoc {
+    uint32_t iC, iW, iE, iN, iS;      // word indices of the cell and its 4 neighbours (one plane)
+    uint32_t iev;                     // index into the per-cell event counters
+    uint32_t gid32;                   // global cell id (Philox counter word 1, R17)
+};
 
-        // ---- a3: stage the closure (cell + one-site halo) into registers ----
-        uint64_t P[NP], h[NP][4], h0[NP][4];
+// Active-cell number t -> cell location.  All indices fit 32 bits (kmc_create enforces < 2^32
+// cells in total, and a plane holds at most that many words plus two ghost rows).
+template <int NDIM>
+__device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
+    const Geo& g = a.g;
+    const uint32_t half = (uint32_t)g.Mx >> 1;
+    const uint32_t j = t % half;
+    const uint32_t rest = t / half;
+    const uint32_t r = rest % (uint32_t)g.R;
+    const uint32_t rowsel = rest / (uint32_t)g.R;
+    uint32_t cy, cx;
+    if (NDIM == 1) {
+        cy = 0;
+        cx = 2 * j + a.colour;
+    } else if (a.C == 2) {
+        cy = rowsel;
+        cx = 2 * j + ((a.colour + g.row_offset + cy) & 1);
+    } else {
+        cy = 2 * rowsel + (a.colour >> 1);
+        cx = 2 * j + (a.colour & 1);
+    }
+    const uint32_t gy = g.row_offset + cy;
+    const uint32_t rowlen = (uint32_t)g.R * g.Mx;
+    const int sy = (int)cy + g.ghost;
+    int syN = sy - 1, syS = sy + 1;
+    if (!g.ghost) {
+        if (syN < 0) syN += g.My_local;
+        if (syS >= g.My_local) syS -= g.My_local;
+    }
+    const uint32_t cxW = cx == 0 ? g.Mx - 1 : cx - 1;
+    const uint32_t cxE = cx == (uint32_t)g.Mx - 1 ? 0 : cx + 1;
+    const uint32_t rbase = r * g.Mx;
+    const uint32_t base = (uint32_t)sy * rowlen + rbase;
+    CellLoc L;
+    L.iC = base + cx;
+    L.iW = base + cxW;
+    L.iE = base + cxE;
+    L.iN = (uint32_t)syN * rowlen + rbase + cx;
+    L.iS = (uint32_t)syS * rowlen + rbase + cx;
+    L.iev = cy * rowlen + rbase + cx;
+    L.gid32 = (uint32_t)((unsigned long long)(g.rep_offset + r) * (unsigned long long)g.M_global +
+                         (unsigned long long)gy * g.Mx + cx);
+    return L;
+}
+
+template <int KIND, int NDIM, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
+    using M = Model<KIND, NDIM>;
+    constexpr int NP = M::NP, NC = M::NC;
+    const Geo& g = a.g;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long cbeg64 = (unsigned long long)warp * chunk;
+    if (cbeg64 >= nactive) return;                                  // warp-uniform
+    const uint32_t cbeg = (uint32_t)cbeg64;
+    const uint32_t cend = (uint32_t)min(cbeg64 + chunk, (unsigned long long)nactive);
+    const uint64_t notcol0 = g.valid & ~g.col0, notcolL = g.valid & ~g.colL;
+    const uint64_t notrow0 = g.valid & ~g.row0, notrowL = g.valid & ~g.rowL;
+    uint64_t* planes[2] = {a.plane0, a.plane1};
+
+    uint32_t next = cbeg + 32;                                      // warp-uniform queue head
+    uint32_t ci = cbeg + lane;
+    bool have = ci < cend;
+    uint32_t gid32 = 0, k = 0;
+    double tclock = 0.0;
+    uint64_t P[NP], h[NP][4];
+    unsigned long long evsum = 0;
+
+    // a3: stage the closure (cell + one-site halo) of cell `ci` into registers
+    auto load = [&](uint32_t c) {
+        const CellLoc L = locate<NDIM>(a, c);
+        gid32 = L.gid32;
+        k = 0;
+        tclock = 0.0;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const uint64_t* pl = planes[p];
-            P[p] = pl[iC];
-            h[p][0] = (pl[iW] >> (g.qx - 1)) & g.col0;           // sigma(x-1) seen by column 0
-            h[p][1] = (pl[iE] << (g.qx - 1)) & g.colL;           // sigma(x+1) seen by column qx-1
+            P[p] = pl[L.iC];
+            h[p][0] = (pl[L.iW] >> (g.qx - 1)) & g.col0;           // sigma(x-1) seen by column 0
+            h[p][1] = (pl[L.iE] << (g.qx - 1)) & g.colL;           // sigma(x+1) seen by column qx-1
             if (NDIM == 2) {
-                h[p][2] = (pl[iN] >> g.shN) & g.row0;             // sigma(y-1) seen by row 0
-                h[p][3] = (pl[iS] << g.shN) & g.rowL;             // sigma(y+1) seen by row qy-1
+                h[p][2] = (pl[L.iN] >> g.shN) & g.row0;             // sigma(y-1) seen by row 0
+                h[p][3] = (pl[L.iS] << g.shN) & g.rowL;             // sigma(y+1) seen by row qy-1
             } else {
                 h[p][2] = h[p][3] = 0;
             }
-#pragma unroll
-            for (int d = 0; d < 4; ++d) h0[p][d] = h[p][d];
         }
-        const uint64_t notcol0 = g.valid & ~g.col0, notcolL = g.valid & ~g.colL;
-        const uint64_t notrow0 = g.valid & ~g.row0, notrowL = g.valid & ~g.rowL;
-        const uint32_t w_lo = a.w_lo, w_hi = a.w_hi_tag, gid32 = (uint32_t)gid;
-        double tclock = 0.0;
+    };
+    // a6: write the cell back once per window (+ halo deltas for hop / pair events)
+    auto store = [&](uint32_t c) {
+        if (k == 0) return;
+        const CellLoc L = locate<NDIM>(a, c);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            uint64_t* pl = planes[p];
+            pl[L.iC] = P[p];
+            if (KIND != 0) {
+                // halo deltas.  Our halo bits of the neighbour words are written by no other cell
+                // in this window (same-colour closures are disjoint, R6), so re-reading them gives
+                // the window-start values; the XOR touches only those bits (order-free).
+                const uint64_t dW = h[p][0] ^ ((pl[L.iW] >> (g.qx - 1)) & g.col0);
+                const uint64_t dE = h[p][1] ^ ((pl[L.iE] << (g.qx - 1)) & g.colL);
+                if (dW) atomicXor((unsigned long long*)&pl[L.iW], (unsigned long long)(dW << (g.qx - 1)));
+                if (dE) atomicXor((unsigned long long*)&pl[L.iE], (unsigned long long)(dE >> (g.qx - 1)));
+                if (NDIM == 2) {
+                    const uint64_t dN = h[p][2] ^ ((pl[L.iN] >> g.shN) & g.row0);
+                    const uint64_t dS = h[p][3] ^ ((pl[L.iS] << g.shN) & g.rowL);
+                    if (dN) atomicXor((unsigned long long*)&pl[L.iN], (unsigned long long)(dN << g.shN));
+                    if (dS) atomicXor((unsigned long long*)&pl[L.iS], (unsigned long long)(dS >> g.shN));
+                }
+            }
+        }
+        a.wev[L.iev] += k;
+        evsum += k;
+    };
 
-        // ---- a5: the per-cell SSA event loop ----
-        for (;;) {
+    if (have) load(ci);
+    while (__any_sync(FULL, have)) {
+        bool fin = false;
+        if (have) {
+            // RNG and -ln U first: independent of lambda, so they overlap the mask chain (ILP)
+            uint4 x = make_uint4(k, gid32, a.w_lo, a.w_hi_tag);
+#pragma unroll
+            for (int rd = 0; rd < 10; ++rd) {
+                const uint32_t lo0 = 0xD2511F53u * x.x, hi0 = __umulhi(0xD2511F53u, x.x);
+                const uint32_t lo1 = 0xCD9E8D57u * x.z, hi1 = __umulhi(0xCD9E8D57u, x.z);
+                x = make_uint4(hi1 ^ x.y ^ a.rk0[rd], lo1, hi0 ^ x.w ^ a.rk1[rd], lo0);
+            }
+            const uint64_t j53 = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
+            const double U = __dmul_rn(__ull2double_rn(j53 + 1ull), 0x1p-53);
+            const double E = -log_spec(U);
+
+            // a4/a5: class masks, counts and lambda (eq.(totalrate), exact u64)
             uint64_t nb[NP][4];
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
@@ -286,91 +367,86 @@ substep_kernel(const SubstepArgs a, const long long nactive) {
                 cnt[c] = __popcll(m[c]);
                 lam += (uint64_t)cnt[c] * a.rate[c];
             }
-            if (lam == 0) break;                                   // quiescent cell
-            const uint4 x = philox4x32_10(make_uint4(k, gid32, w_lo, w_hi), a.key0, a.key1);
-            const uint64_t j53 = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
-            const double U = __dmul_rn(__ull2double_rn(j53 + 1ull), 0x1p-53);
-            const double E = -log_spec(U);
             const double lamd = __dmul_rn(__ull2double_rn(lam), a.inv_scale);
             const double tau = __ddiv_rn(E, lamd);
             const double tn = __dadd_rn(tclock, tau);
-            if (tn >= a.D) break;                                  // R5: pending event discarded
-            tclock = tn;
-            // class: smallest c with prefix(c) > r, r = floor(x2 * lambda / 2^32)
-            const uint64_t rr = (uint64_t)x.z * (lam >> 32) + (uint64_t)__umulhi(x.z, (uint32_t)lam);
-            uint64_t cum = 0, selm = m[NC - 1];
-            uint32_t selc = cnt[NC - 1];
-            int seld = M::desc(NC - 1);
-            bool found = false;
+            if (lam == 0 || tn >= a.D) {                           // quiescent, or R5 (pending event discarded)
+                fin = true;
+            } else {
+                tclock = tn;
+                // eq.(skeleton): class = smallest c with prefix(c) > r, r = floor(x2 lambda / 2^32)
+                const uint64_t rr = (uint64_t)x.z * (lam >> 32) + (uint64_t)__umulhi(x.z, (uint32_t)lam);
+                uint64_t cum = 0, selm = m[NC - 1];
+                uint32_t selc = cnt[NC - 1];
+                int seld = M::desc(NC - 1);
+                bool found = false;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                cum += (uint64_t)cnt[c] * a.rate[c];
-                const bool hit = !found && cum > rr;
-                if (hit) { selm = m[c]; selc = cnt[c]; seld = M::desc(c); }
-                found = found || hit;
-            }
-            // site: the kk-th member of the class in row-major order, kk = floor(x3 * cnt / 2^32)
-            const uint32_t kk = __umulhi(x.w, selc);
-            const int s = select_bit64(selm, kk);
-            const uint64_t ab = 1ull << s;
-            if (seld & D_A0) P[0] ^= ab;
-            if (NP > 1 && (seld & D_A1)) P[NP - 1] ^= ab;
-            if (seld & D_HASP) {
-                const int d = (seld >> 4) & 3;
-                uint64_t inner, pb;
-                if (d == 0)      { inner = notcol0; pb = ab >> 1; }
-                else if (d == 1) { inner = notcolL; pb = ab << 1; }
-                else if (d == 2) { inner = notrow0; pb = ab >> g.qx; }
-                else             { inner = notrowL; pb = ab << g.qx; }
-                const bool in_cell = (ab & inner) != 0;
+                for (int c = 0; c < NC; ++c) {
+                    cum += (uint64_t)cnt[c] * a.rate[c];
+                    const bool hit = !found && cum > rr;
+                    if (hit) { selm = m[c]; selc = cnt[c]; seld = M::desc(c); }
+                    found = found || hit;
+                }
+                // site: the kk-th member of the class in row-major order, kk = floor(x3 cnt / 2^32)
+                const int s = select_bit64(selm, __umulhi(x.w, selc));
+                const uint64_t ab = 1ull << s;
+                if (seld & D_A0) P[0] ^= ab;
+                if (NP > 1 && (seld & D_A1)) P[NP - 1] ^= ab;
+                if (seld & D_HASP) {
+                    const int d = (seld >> 4) & 3;
+                    uint64_t inner, pb;
+                    if (d == 0)      { inner = notcol0; pb = ab >> 1; }
+                    else if (d == 1) { inner = notcolL; pb = ab << 1; }
+                    else if (d == 2) { inner = notrow0; pb = ab >> g.qx; }
+                    else             { inner = notrowL; pb = ab << g.qx; }
+                    const bool in_cell = (ab & inner) != 0;
 #pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    if (seld & (D_P0 << p)) {
-                        if (in_cell) P[p] ^= pb;
-                        else {
+                    for (int p = 0; p < NP; ++p) {
+                        if (seld & (D_P0 << p)) {
+                            if (in_cell) P[p] ^= pb;
+                            else {
 #pragma unroll
-                            for (int dd = 0; dd < 4; ++dd)
-                                if (dd == d) h[p][dd] ^= ab;
+                                for (int dd = 0; dd < 4; ++dd)
+                                    if (dd == d) h[p][dd] ^= ab;
+                            }
                         }
                     }
                 }
+                ++k;
             }
-            ++k;
         }
-
-        // ---- a6: write back once per window ----
-        if (k) {
-#pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                uint64_t* pl = planes[p];
-                pl[iC] = P[p];
-                if (KIND != 0) {   // halo deltas (pair / hop events): disjoint bits, order-free XOR
-                    const uint64_t dW = h[p][0] ^ h0[p][0], dE = h[p][1] ^ h0[p][1];
-                    if (dW) atomicXor((unsigned long long*)&pl[iW], (unsigned long long)(dW << (g.qx - 1)));
-                    if (dE) atomicXor((unsigned long long*)&pl[iE], (unsigned long long)(dE >> (g.qx - 1)));
-                    if (NDIM == 2) {
-                        const uint64_t dN = h[p][2] ^ h0[p][2], dS = h[p][3] ^ h0[p][3];
-                        if (dN) atomicXor((unsigned long long*)&pl[iN], (unsigned long long)(dN << g.shN));
-                        if (dS) atomicXor((unsigned long long*)&pl[iS], (unsigned long long)(dS >> g.shN));
-                    }
-                }
+        const unsigned fm = __ballot_sync(FULL, fin);
+        if (fm) {
+            if (fin) {
+                store(ci);
+                ci = next + __popc(fm & ((1u << lane) - 1u));
+                have = ci < cend;
+                if (have) load(ci);
             }
-            a.wev[(long long)cy * rowlen + (long long)r * g.Mx + cx] += k;
+            next += __popc(fm);
         }
     }
     // event total: warp-aggregated
-    unsigned long long kw = k;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kw += __shfl_xor_sync(0xffffffffu, kw, o);
-    if ((threadIdx.x & 31) == 0 && kw) atomicAdd(a.ev_total, kw);
+    for (int o = 16; o > 0; o >>= 1) evsum += __shfl_xor_sync(FULL, evsum, o);
+    if (lane == 0 && evsum) atomicAdd(a.ev_total, evsum);
 }
 
 template <int KIND, int NDIM>
 static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
     if (nactive <= 0) return cudaSuccess;
     const int bs = 256;
-    const long long nb = (nactive + bs - 1) / bs;
-    substep_kernel<KIND, NDIM><<<(unsigned)nb, bs, 0, s>>>(a, nactive);
+    // cells per warp: 32 lanes x a few cells each, so a lane's tail idles for ~1/cpl of the window
+    long long cpl = 8;
+    while (cpl > 1 && (nactive + 32 * cpl - 1) / (32 * cpl) < 4 * 148 * 8) cpl >>= 1;   // keep >= ~4 waves
+    const long long chunk = 32 * cpl;
+    const long long nwarps = (nactive + chunk - 1) / chunk;
+    const long long nb = (nwarps * 32 + bs - 1) / bs;
+    static const int minb_env = [] { const char* e = getenv("KMC_MINB"); return e ? atoi(e) : 0; }();
+    if (KIND == 0 && minb_env != 2)
+        substep_kernel<KIND, NDIM, 3><<<(unsigned)nb, bs, 0, s>>>(a, (uint32_t)nactive, (uint32_t)chunk);
+    else
+        substep_kernel<KIND, NDIM, 2><<<(unsigned)nb, bs, 0, s>>>(a, (uint32_t)nactive, (uint32_t)chunk);
     return cudaGetLastError();
 }
 
