@@ -56,8 +56,8 @@ void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint3
 }
 
 /* ------------------------------------------------------------------ */
-/* L0: natural log, the fdlibm e_log.c operation sequence (IEEE basic  */
-/* operations only, no contraction).  Domain used: x in [2^-53, 1].    */
+/* L0: natural log, the fdlibm e_log.c general-path operation sequence */
+/* (IEEE basic operations only, no contraction).  Domain: [2^-1022, 1]. */
 /* ------------------------------------------------------------------ */
 static const double ln2_hi = 0x1.62e42feep-1;          /* 3fe62e42 fee00000 */
 static const double ln2_lo = 0x1.a39ef35793c76p-33;    /* 3dea39ef 35793c76 */
@@ -74,55 +74,26 @@ static inline double bitsd(uint64_t u) { double x; memcpy(&x, &u, 8); return x; 
 
 double orc_log(double x)
 {
+    /* the fdlibm e_log.c reduction and polynomial, evaluated with its single
+     * general formula for every x in the domain (no special-case branches). */
     uint64_t u = dbits(x);
     int32_t hx = (int32_t)(u >> 32);
-    uint32_t lx = (uint32_t)u;
-    int32_t k = 0;
-    if (hx < 0x00100000) {                    /* x < 2^-1022 */
-        if (((hx & 0x7fffffff) | (int32_t)lx) == 0) return -INFINITY;
-        if (hx < 0) return NAN;
-        k -= 54;
-        x *= 0x1p54;                          /* subnormal: scale up */
-        u = dbits(x);
-        hx = (int32_t)(u >> 32);
-    }
-    if (hx >= 0x7ff00000) return x + x;
-    k += (hx >> 20) - 1023;
+    if (x == 0.0) return -INFINITY;
+    if (hx < 0x00100000 || hx >= 0x7ff00000) return NAN;   /* outside the specified domain */
+    int32_t k = (hx >> 20) - 1023;
     hx &= 0x000fffff;
     int32_t i = (hx + 0x95f64) & 0x100000;
-    u = dbits(x);
     u = ((uint64_t)(uint32_t)(hx | (i ^ 0x3ff00000)) << 32) | (u & 0xffffffffu);
     x = bitsd(u);                             /* x or x/2 normalised to [sqrt(2)/2, sqrt(2)) */
     k += (i >> 20);
     double f = x - 1.0;
-    double dk;
-    if ((0x000fffff & (2 + hx)) < 3) {        /* -2^-20 <= f < 2^-20 */
-        if (f == 0.0) {
-            if (k == 0) return 0.0;
-            dk = (double)k;
-            return dk * ln2_hi + dk * ln2_lo;
-        }
-        double R = f * f * (0.5 - 0.33333333333333333 * f);
-        if (k == 0) return f - R;
-        dk = (double)k;
-        return dk * ln2_hi - ((R - dk * ln2_lo) - f);
-    }
+    double dk = (double)k;
     double s = f / (2.0 + f);
-    dk = (double)k;
     double z = s * s;
-    i = hx - 0x6147a;
     double w = z * z;
-    int32_t j = 0x6b851 - hx;
     double t1 = w * (Lg2 + w * (Lg4 + w * Lg6));
     double t2 = z * (Lg1 + w * (Lg3 + w * (Lg5 + w * Lg7)));
-    i |= j;
     double R = t2 + t1;
-    if (i > 0) {
-        double hfsq = 0.5 * f * f;
-        if (k == 0) return f - (hfsq - s * (hfsq + R));
-        return dk * ln2_hi - ((hfsq - (s * (hfsq + R) + dk * ln2_lo)) - f);
-    }
-    if (k == 0) return f - s * (f - R);
     return dk * ln2_hi - ((s * (f - R) - dk * ln2_lo) - f);
 }
 

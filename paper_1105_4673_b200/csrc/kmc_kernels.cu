@@ -39,8 +39,10 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
     return c;
 }
 
-// natural log on [2^-53, 1] (normal inputs only), fdlibm e_log.c operation order, every
-// operation an explicit round-to-nearest intrinsic so nvcc cannot contract to FMA.
+// natural log on [2^-53, 1] (normal inputs only): the fdlibm e_log.c argument reduction and
+// polynomial with its single general formula (no special-case branches, so a
+// warp never diverges here); every operation an explicit round-to-nearest intrinsic so nvcc
+// cannot contract to FMA.
 __device__ __forceinline__ double log_spec(double x) {
     const double ln2_hi = 0x1.62e42feep-1, ln2_lo = 0x1.a39ef35793c76p-33;
     const double Lg1 = 0x1.5555555555593p-1, Lg2 = 0x1.999999997fa04p-2, Lg3 = 0x1.2492494229359p-2;
@@ -50,36 +52,17 @@ __device__ __forceinline__ double log_spec(double x) {
     const int lx = __double2loint(x);
     int k = (hx >> 20) - 1023;
     hx &= 0x000fffff;
-    int i = (hx + 0x95f64) & 0x100000;
+    const int i = (hx + 0x95f64) & 0x100000;
     const double xn = __hiloint2double(hx | (i ^ 0x3ff00000), lx);
     k += (i >> 20);
     const double f = __dsub_rn(xn, 1.0);
     const double dk = (double)k;
-    if ((0x000fffff & (2 + hx)) < 3) {
-        if (f == 0.0) {
-            if (k == 0) return 0.0;
-            return __dadd_rn(__dmul_rn(dk, ln2_hi), __dmul_rn(dk, ln2_lo));
-        }
-        const double R = __dmul_rn(__dmul_rn(f, f), __dsub_rn(0.5, __dmul_rn(0.33333333333333333, f)));
-        if (k == 0) return __dsub_rn(f, R);
-        return __dsub_rn(__dmul_rn(dk, ln2_hi), __dsub_rn(__dsub_rn(R, __dmul_rn(dk, ln2_lo)), f));
-    }
     const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
     const double z = __dmul_rn(s, s);
-    i = hx - 0x6147a;
     const double w = __dmul_rn(z, z);
-    const int j = 0x6b851 - hx;
     const double t1 = __dmul_rn(w, __dadd_rn(Lg2, __dmul_rn(w, __dadd_rn(Lg4, __dmul_rn(w, Lg6)))));
     const double t2 = __dmul_rn(z, __dadd_rn(Lg1, __dmul_rn(w, __dadd_rn(Lg3, __dmul_rn(w, __dadd_rn(Lg5, __dmul_rn(w, Lg7)))))));
-    i |= j;
     const double R = __dadd_rn(t2, t1);
-    if (i > 0) {
-        const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
-        if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, __dmul_rn(s, __dadd_rn(hfsq, R))));
-        return __dsub_rn(__dmul_rn(dk, ln2_hi),
-                         __dsub_rn(__dsub_rn(hfsq, __dadd_rn(__dmul_rn(s, __dadd_rn(hfsq, R)), __dmul_rn(dk, ln2_lo))), f));
-    }
-    if (k == 0) return __dsub_rn(f, __dmul_rn(s, __dsub_rn(f, R)));
     return __dsub_rn(__dmul_rn(dk, ln2_hi), __dsub_rn(__dsub_rn(__dmul_rn(s, __dsub_rn(f, R)), __dmul_rn(dk, ln2_lo)), f));
 }
 
