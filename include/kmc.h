@@ -159,6 +159,18 @@ kmc_status kmc_timing(kmc_ctx* ctx, double* kernel_ms, int64_t* launches, int32_
  * out[3] = rows_local, out[4] = rank above (-y neighbour, -1 if none), out[5] = rank below. */
 kmc_status kmc_partition_plan(const kmc_geometry* geom, int32_t kind, int32_t world, int32_t rank, int64_t out[6]);
 
+/* Virtual ranks (single-GPU check of the multi-GPU path): create `world` contexts (ranks 0..world-1,
+ * out[world]) holding the slabs of ONE 2D lattice on one device and stream, with exactly the slab
+ * layout, ghost rows and exchange protocol of the NCCL path but the halo rows moved
+ * by stream-ordered device copies.  kmc_vgroup_run advances all of them in lockstep (kmc_run and
+ * kmc_substep on these contexts return KMC_ESTATE); kmc_vgroup_sync refreshes the ghost rows (call
+ * it before kmc_observables, which then returns this rank's local counts, not the group sum).
+ * Results are bit-identical to world = 1 (global ids).  Destroy each context with kmc_destroy. */
+kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, int32_t world, int32_t device,
+                             void* stream, kmc_ctx** out);
+kmc_status kmc_vgroup_run(kmc_ctx** ctxs, int32_t world, double T, double dt, kmc_scheme scheme);
+kmc_status kmc_vgroup_sync(kmc_ctx** ctxs, int32_t world);
+
 /* NCCL unique id for world > 1 (rank 0 calls it and broadcasts the 128 bytes). */
 kmc_status kmc_nccl_unique_id(uint8_t out[128]);
 

@@ -144,6 +144,15 @@ def law(p0, Q, Qc, scheme, dt, T, C):
     return p
 
 
+def law_sequence(p0, Qc, seq):
+    """Exact law after the given window sequence [(colour, duration), ...]: p0 prod e^{d Q^c}
+    (e.g. one realisation xi_1, xi_2, ... of the random schedule, eq.(SL))."""
+    p = p0.copy()
+    for c, d in seq:
+        p = evolve(p, Qc[c], d)
+    return p
+
+
 def coverage_values(lat, S, state=1, sites=None):
     """Per-configuration coverage of `state` (fraction of `sites`, default all)."""
     N = lat.N

@@ -26,7 +26,7 @@ EXPORTS = [
     "kmc_set_config", "kmc_get_config", "kmc_set_config_device", "kmc_get_config_device",
     "kmc_run", "kmc_substep", "kmc_observables", "kmc_get_state", "kmc_set_state",
     "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
-    "kmc_nccl_unique_id", "kmc_version",
+    "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
 ]
 
 
@@ -93,6 +93,9 @@ def lib():
         "kmc_partition_plan": ([P(KmcGeometry), i32, i32, i32, vp], i32),
         "kmc_nccl_unique_id": ([vp], i32),
         "kmc_version": ([], ctypes.c_char_p),
+        "kmc_vgroup_create": ([P(KmcGeometry), P(KmcModel), i32, i32, vp, vp], i32),
+        "kmc_vgroup_run": ([vp, i32, dbl, dbl, i32], i32),
+        "kmc_vgroup_sync": ([vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -264,3 +267,79 @@ class KMC:
         ms, n = ctypes.c_double(), ctypes.c_int64()
         self._check(self._L.kmc_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
         return ms.value, n.value
+
+
+class _Rank(KMC):
+    """One virtual rank of a VGroup (created by kmc_vgroup_create, not kmc_create)."""
+
+    def __init__(self, L, ctx, kind, geom, model):
+        self._L = L
+        self._ctx = ctx
+        self.kind = kind
+        self.nstates = NSTATES[kind]
+        self.geom = geom
+        self.model = model
+        rl, hl, w, ro, yo = (ctypes.c_int64() for _ in range(5))
+        self._check(L.kmc_local_shape(ctx, ctypes.byref(rl), ctypes.byref(hl), ctypes.byref(w),
+                                      ctypes.byref(ro), ctypes.byref(yo)))
+        self.local_shape = (rl.value, hl.value, w.value)
+        self.replica_offset, self.row_offset = ro.value, yo.value
+        self.nbytes = rl.value * hl.value * w.value
+
+
+class VGroup:
+    """`world` virtual ranks of one 2D lattice on one GPU (kmc_vgroup_*): the multi-GPU slab
+    decomposition and halo-exchange protocol, with stream-ordered copies instead of NCCL."""
+
+    def __init__(self, world, dims, cell, kind="adsdes", colours=0, replicas=1, seed=0, device=0,
+                 stream=None, **params):
+        L = lib()
+        self._L = L
+        self.world = int(world)
+        k = KINDS[kind] if isinstance(kind, str) else int(kind)
+        self.geom = make_geometry(2, dims, cell, colours, replicas, seed)
+        self.model = make_model(k, **params)
+        arr = (ctypes.c_void_p * self.world)()
+        st = L.kmc_vgroup_create(ctypes.byref(self.geom), ctypes.byref(self.model), self.world, int(device),
+                                 stream, arr)
+        if st != KMC_OK:
+            raise KmcError(st, L.kmc_create_error().decode())
+        self._arr = arr
+        self.ranks = [_Rank(L, ctypes.c_void_p(arr[r]), k, self.geom, self.model) for r in range(self.world)]
+
+    def _check(self, st, allow=()):
+        if st != KMC_OK and st not in allow:
+            raise KmcError(st, self._L.kmc_last_error(self.ranks[0]._ctx).decode())
+        return st
+
+    def set_config(self, lat):
+        """Full lattice [replicas][H][W] -> each rank's slab."""
+        lat = np.ascontiguousarray(lat, dtype=np.uint8)
+        for rk in self.ranks:
+            h = rk.local_shape[1]
+            rk.set_config(lat[:, rk.row_offset:rk.row_offset + h])
+
+    def get_config(self):
+        return np.concatenate([rk.get_config() for rk in self.ranks], axis=1)
+
+    def run(self, T, dt, scheme="lie"):
+        sc = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+        return self._check(self._L.kmc_vgroup_run(self._arr, self.world, float(T), float(dt), sc),
+                           allow=(KMC_WTRUNCATED,)) == KMC_WTRUNCATED
+
+    def observables(self):
+        """Group sum of the integer counters (ghost rows refreshed first)."""
+        self._check(self._L.kmc_vgroup_sync(self._arr, self.world))
+        obs = [rk.observables() for rk in self.ranks]
+        out = dict(obs[0])
+        for key in ("n_state", "nn_pairs", "n_state_by_colour"):
+            out[key] = sum(o[key] for o in obs)
+        out["events"] = sum(o["events"] for o in obs)
+        n = out["n_state"].sum()
+        out["coverage"] = out["n_state"] / n
+        out["energy"] = -self.model.K * float(out["nn_pairs"][1, 1]) + self.model.h * float(out["n_state"][1])
+        return out
+
+    def close(self):
+        for rk in self.ranks:
+            rk.close()

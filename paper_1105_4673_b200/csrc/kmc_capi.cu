@@ -111,6 +111,7 @@ struct kmc_ctx {
     unsigned long long* h_obs = nullptr;     // pinned
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
     // schedule state
     uint64_t window = 0;
     double time = 0.0;
@@ -214,7 +215,7 @@ long long active_cells(const kmc_ctx* c) {
 
 // a7 forward exchange (world > 1, 2D): owned boundary cell rows -> neighbours' ghost rows.
 kmc_status exchange_forward(kmc_ctx* c) {
-    if (c->world == 1 || c->g.ndim == 1) return KMC_OK;
+    if (c->world == 1 || c->g.ndim == 1 || !c->comm) return KMC_OK;   // vgroup: exchanged by its driver
     const size_t rowlen = (size_t)c->g.R * c->g.Mx;
     const int My = c->g.My_local;
     NCCL_TRY(c, g_nccl.GroupStart());
@@ -241,7 +242,7 @@ kmc_status exchange_forward(kmc_ctx* c) {
 // a7 reverse exchange for cross-cell-writing models: ghost-row deltas back to their owners,
 // merged by XOR (same-colour closures are disjoint, R6, so exactly one writer per bit).
 kmc_status exchange_reverse(kmc_ctx* c) {
-    if (c->world == 1 || c->g.ndim == 1 || !c->cross) return KMC_OK;
+    if (c->world == 1 || c->g.ndim == 1 || !c->cross || !c->comm) return KMC_OK;
     const size_t rowlen = (size_t)c->g.R * c->g.Mx;
     const int My = c->g.My_local;
     for (int p = 0; p < c->nplanes; ++p) {   // snap := ghost XOR snap  (the delta)
@@ -268,11 +269,8 @@ kmc_status exchange_reverse(kmc_ctx* c) {
     return KMC_OK;
 }
 
-kmc_status do_substep(kmc_ctx* c, int colour, double D) {
-    if (colour < 0 || colour >= c->C) return fail(c, KMC_EINVAL, "colour %d out of range [0,%d)", colour, c->C);
-    if (!(D >= 0.0)) return fail(c, KMC_EINVAL, "window duration must be >= 0");
-    kmc_status st = exchange_forward(c);
-    if (st != KMC_OK) return st;
+// One window's kernel (a3-a6) on this rank's owned cells of `colour`; advances the window counter.
+kmc_status launch_window(kmc_ctx* c, int colour, double D) {
     SubstepArgs a{};
     a.g = c->g;
     a.plane0 = c->planes[0];
@@ -308,6 +306,16 @@ kmc_status do_substep(kmc_ctx* c, int colour, double D) {
     CUDA_TRY(c, launch_substep(c->kind, a, active_cells(c), c->stream));
     if (c->timing) CUDA_TRY(c, cudaEventRecord(e1, c->stream));
     c->window += 1;
+    return KMC_OK;
+}
+
+kmc_status do_substep(kmc_ctx* c, int colour, double D) {
+    if (colour < 0 || colour >= c->C) return fail(c, KMC_EINVAL, "colour %d out of range [0,%d)", colour, c->C);
+    if (!(D >= 0.0)) return fail(c, KMC_EINVAL, "window duration must be >= 0");
+    kmc_status st = exchange_forward(c);
+    if (st != KMC_OK) return st;
+    st = launch_window(c, colour, D);
+    if (st != KMC_OK) return st;
     return exchange_reverse(c);
 }
 
@@ -317,11 +325,90 @@ int random_colour(uint64_t seed, uint64_t w, int C) {
     return (int)(((uint64_t)C * ctr[0]) >> 32);
 }
 
+// a2: the sub-steps (colour, duration) of one macro-step of duration d starting at window w0.
+std::vector<std::pair<int, double>> macro_schedule(int scheme, int C, double d, uint64_t seed, uint64_t w0) {
+    std::vector<std::pair<int, double>> s;
+    const double h = d * 0.5;
+    if (scheme == KMC_LIE) {                        // eq.(lie), colour 0 first (R1)
+        for (int col = 0; col < C; ++col) s.emplace_back(col, d);
+    } else if (scheme == KMC_STRANG) {              // eq.(strang), halves to colour 0 (R2)
+        if (C == 2) s = {{0, h}, {1, d}, {0, h}};
+        else s = {{0, h}, {1, h}, {2, h}, {3, d}, {2, h}, {1, h}, {0, h}};
+    } else {                                        // eq.(SLPCS): C windows, xi_w by window id (R4)
+        for (int k = 0; k < C; ++k) s.emplace_back(random_colour(seed, w0 + (uint64_t)k, C), d);
+    }
+    return s;
+}
+
+// R20: macro-step durations of kmc_run(T, dt).
+std::vector<double> macro_durations(double T, double dt, bool* truncated) {
+    std::vector<double> out;
+    *truncated = false;
+    if (T == 0.0) return out;
+    long long n = (long long)std::ceil(T / dt - 1e-9);
+    if (n < 1) n = 1;
+    double last = T - (double)(n - 1) * dt;
+    *truncated = true;
+    if (std::fabs(last - dt) <= 1e-9 * dt) { last = dt; *truncated = false; }
+    out.assign((size_t)n, dt);
+    out.back() = last;
+    return out;
+}
+
+// ---- virtual ranks: G slabs of one lattice on one device, exchanged by stream-ordered copies ----
+// Same partition and exchange protocol as the NCCL path (exchange_forward / exchange_reverse), run
+// in lockstep by one host thread, so the multi-rank logic can be checked on a single GPU.
+kmc_status vgroup_forward(kmc_ctx** cs, int world) {
+    for (int r = 0; r < world; ++r) {
+        kmc_ctx* c = cs[r];
+        const size_t rowlen = (size_t)c->g.R * c->g.Mx;
+        const int My = c->g.My_local;
+        kmc_ctx* up = cs[c->rank_up];
+        kmc_ctx* dn = cs[c->rank_down];
+        for (int p = 0; p < c->nplanes; ++p) {
+            CUDA_TRY(c, cudaMemcpyAsync(c->planes[p], up->planes[p] + (size_t)up->g.My_local * rowlen, rowlen * 8,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_TRY(c, cudaMemcpyAsync(c->planes[p] + (size_t)(My + 1) * rowlen, dn->planes[p] + rowlen, rowlen * 8,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+            if (c->cross) {
+                CUDA_TRY(c, cudaMemcpyAsync(c->ghost_snap + (size_t)(2 * p) * rowlen, c->planes[p], rowlen * 8,
+                                            cudaMemcpyDeviceToDevice, c->stream));
+                CUDA_TRY(c, cudaMemcpyAsync(c->ghost_snap + (size_t)(2 * p + 1) * rowlen, c->planes[p] + (size_t)(My + 1) * rowlen,
+                                            rowlen * 8, cudaMemcpyDeviceToDevice, c->stream));
+            }
+        }
+    }
+    return KMC_OK;
+}
+
+kmc_status vgroup_reverse(kmc_ctx** cs, int world) {
+    for (int r = 0; r < world; ++r) {
+        kmc_ctx* c = cs[r];
+        if (!c->cross) return KMC_OK;
+        const size_t rowlen = (size_t)c->g.R * c->g.Mx;
+        const int My = c->g.My_local;
+        kmc_ctx* up = cs[c->rank_up];
+        kmc_ctx* dn = cs[c->rank_down];
+        for (int p = 0; p < c->nplanes; ++p) {
+            uint64_t* dtop = c->ghost_snap + (size_t)(2 * p) * rowlen;
+            uint64_t* dbot = c->ghost_snap + (size_t)(2 * p + 1) * rowlen;
+            CUDA_TRY(c, launch_xor_rows(dtop, c->planes[p], nullptr, (long long)rowlen, c->stream));
+            CUDA_TRY(c, launch_xor_rows(dbot, c->planes[p] + (size_t)(My + 1) * rowlen, nullptr, (long long)rowlen, c->stream));
+            CUDA_TRY(c, launch_xor_rows(up->planes[p] + (size_t)up->g.My_local * rowlen, dtop, nullptr, (long long)rowlen, c->stream));
+            CUDA_TRY(c, launch_xor_rows(dn->planes[p] + rowlen, dbot, nullptr, (long long)rowlen, c->stream));
+        }
+    }
+    return KMC_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------------------------
+static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, const kmc_dist* dist, bool vgroup,
+                             kmc_ctx** out);
+
 extern "C" {
 
 const char* kmc_version(void) { return KMC_VERSION; }
@@ -363,6 +450,13 @@ kmc_status kmc_nccl_unique_id(uint8_t out[128]) {
 }
 
 kmc_status kmc_create(const kmc_geometry* geom, const kmc_model* model, const kmc_dist* dist, kmc_ctx** out) {
+    return create_ctx(geom, model, dist, false, out);
+}
+
+}  // extern "C"
+
+static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, const kmc_dist* dist, bool vgroup,
+                             kmc_ctx** out) {
     if (!out) return fail(nullptr, KMC_EINVAL, "NULL out");
     *out = nullptr;
     if (!geom || !model) return fail(nullptr, KMC_EINVAL, "NULL geometry or model");
@@ -461,7 +555,8 @@ kmc_status kmc_create(const kmc_geometry* geom, const kmc_model* model, const km
     e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) { kmc_destroy(c); return fail(nullptr, KMC_ECUDA, "init: %s", cudaGetErrorString(e)); }
 
-    if (world > 1) {
+    c->vgroup = vgroup;
+    if (world > 1 && !vgroup) {
         std::string why;
         if (!dist->nccl_unique_id) { kmc_destroy(c); return fail(nullptr, KMC_EINVAL, "world > 1 needs nccl_unique_id"); }
         if (!load_nccl(&why)) { kmc_destroy(c); return fail(nullptr, KMC_ENCCL, "%s", why.c_str()); }
@@ -473,6 +568,8 @@ kmc_status kmc_create(const kmc_geometry* geom, const kmc_model* model, const km
     *out = c;
     return KMC_OK;
 }
+
+extern "C" {
 
 void kmc_destroy(kmc_ctx* c) {
     if (!c) return;
@@ -560,6 +657,7 @@ kmc_status kmc_get_config(kmc_ctx* c, uint8_t* host, int64_t nbytes) {
 
 kmc_status kmc_substep(kmc_ctx* c, int32_t colour, double duration) {
     if (!c) return KMC_EINVAL;
+    if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: use kmc_vgroup_run");
     CUDA_TRY(c, cudaSetDevice(c->device));
     return do_substep(c, colour, duration);
 }
@@ -568,35 +666,60 @@ kmc_status kmc_run(kmc_ctx* c, double T, double dt, kmc_scheme scheme) {
     if (!c) return KMC_EINVAL;
     if (!(dt > 0.0) || !(T >= 0.0) || std::isinf(T)) return fail(c, KMC_EINVAL, "need dt > 0 and finite T >= 0");
     if (scheme < KMC_LIE || scheme > KMC_RANDOM) return fail(c, KMC_EINVAL, "unknown scheme %d", (int)scheme);
+    if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: use kmc_vgroup_run");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    if (T == 0.0) return KMC_OK;
-    // R20: n = ceil(T/dt - 1e-9) macro-steps, the last of duration T - (n-1) dt
-    long long n = (long long)std::ceil(T / dt - 1e-9);
-    if (n < 1) n = 1;
-    double last = T - (double)(n - 1) * dt;
-    bool truncated = true;
-    if (std::fabs(last - dt) <= 1e-9 * dt) { last = dt; truncated = false; }
-    for (long long i = 0; i < n; ++i) {
-        const double d = (i == n - 1) ? last : dt;
-        const double h = d * 0.5;
-        kmc_status st = KMC_OK;
-        if (scheme == KMC_LIE) {                       // eq.(lie), colour 0 first (R1)
-            for (int col = 0; col < c->C && st == KMC_OK; ++col) st = do_substep(c, col, d);
-        } else if (scheme == KMC_STRANG) {             // eq.(strang), halves to colour 0 (R2)
-            if (c->C == 2) {
-                const int cs[3] = {0, 1, 0};
-                const double ds[3] = {h, d, h};
-                for (int k = 0; k < 3 && st == KMC_OK; ++k) st = do_substep(c, cs[k], ds[k]);
-            } else {
-                const int cs[7] = {0, 1, 2, 3, 2, 1, 0};
-                const double ds[7] = {h, h, h, d, h, h, h};
-                for (int k = 0; k < 7 && st == KMC_OK; ++k) st = do_substep(c, cs[k], ds[k]);
-            }
-        } else {                                       // eq.(SLPCS): C windows, xi_w by window id (R4)
-            for (int k = 0; k < c->C && st == KMC_OK; ++k) st = do_substep(c, random_colour(c->geom.seed, c->window, c->C), d);
+    bool truncated = false;
+    for (double d : macro_durations(T, dt, &truncated)) {
+        for (const auto& sd : macro_schedule(scheme, c->C, d, c->geom.seed, c->window)) {
+            kmc_status st = do_substep(c, sd.first, sd.second);
+            if (st != KMC_OK) return st;
         }
-        if (st != KMC_OK) return st;
         c->time += d;
+    }
+    return truncated ? KMC_WTRUNCATED : KMC_OK;
+}
+
+kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, int32_t world, int32_t device,
+                             void* stream, kmc_ctx** out) {
+    if (!geom || !model || !out || world < 2) return fail(nullptr, KMC_EINVAL, "vgroup needs world >= 2");
+    if (geom->ndim != 2) return fail(nullptr, KMC_EINVAL, "vgroup: 2D lattices only (1D shards replicas)");
+    for (int r = 0; r < world; ++r) out[r] = nullptr;
+    for (int r = 0; r < world; ++r) {
+        kmc_dist d{};
+        d.rank = r; d.world = world; d.device = device; d.stream = stream; d.nccl_unique_id = nullptr;
+        kmc_status st = create_ctx(geom, model, &d, true, &out[r]);
+        if (st != KMC_OK) {
+            for (int q = 0; q < r; ++q) { kmc_destroy(out[q]); out[q] = nullptr; }
+            return st;
+        }
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_vgroup_sync(kmc_ctx** cs, int32_t world) {
+    if (!cs || world < 2) return KMC_EINVAL;
+    CUDA_TRY(cs[0], cudaSetDevice(cs[0]->device));
+    return vgroup_forward(cs, world);
+}
+
+kmc_status kmc_vgroup_run(kmc_ctx** cs, int32_t world, double T, double dt, kmc_scheme scheme) {
+    if (!cs || world < 2) return KMC_EINVAL;
+    kmc_ctx* c0 = cs[0];
+    for (int r = 0; r < world; ++r)
+        if (!cs[r] || !cs[r]->vgroup || cs[r]->world != world || cs[r]->rank != r)
+            return fail(c0, KMC_EINVAL, "vgroup: contexts must be ranks 0..world-1 of one kmc_vgroup_create");
+    if (!(dt > 0.0) || !(T >= 0.0) || std::isinf(T)) return fail(c0, KMC_EINVAL, "need dt > 0 and finite T >= 0");
+    if (scheme < KMC_LIE || scheme > KMC_RANDOM) return fail(c0, KMC_EINVAL, "unknown scheme %d", (int)scheme);
+    CUDA_TRY(c0, cudaSetDevice(c0->device));
+    bool truncated = false;
+    for (double d : macro_durations(T, dt, &truncated)) {
+        for (const auto& sd : macro_schedule(scheme, c0->C, d, c0->geom.seed, c0->window)) {
+            kmc_status st = vgroup_forward(cs, world);
+            for (int r = 0; r < world && st == KMC_OK; ++r) st = launch_window(cs[r], sd.first, sd.second);
+            if (st == KMC_OK) st = vgroup_reverse(cs, world);
+            if (st != KMC_OK) return st;
+        }
+        for (int r = 0; r < world; ++r) cs[r]->time += d;
     }
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }

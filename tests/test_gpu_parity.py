@@ -222,3 +222,31 @@ def test_full_size_sampled_cells(kind):
         assert np.array_equal(post[0, ys, xs], got[0, ys, xs]), (cy, cx)
         assert int(ev_post[cy, cx]) - int(ev_pre[cy, cx]) == int(k), (cy, cx)
     assert ev.sum() > 0
+
+
+@pytest.mark.parametrize("kind,params,scheme,dt,cell", [
+    ("adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), "lie", 1.0, (8, 8)),
+    ("adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), "strang", 0.5, (4, 4)),
+    ("zgb", dict(k1=0.45, k2=1.0), "random", 0.5, (2, 4)),
+])
+@pytest.mark.parametrize("world", [2, 4])
+def test_virtual_ranks_bit_identical(kind, params, scheme, dt, cell, world):
+    """slabs + halo exchange (+ reverse XOR deltas) on G virtual ranks of one GPU give
+    the bit-identical lattice, event counts and observables of G = 1 (global ids)."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    dims = (64, 32)
+    one = kmc.KMC(2, dims, cell, kind=kind, seed=33, replicas=2, **params)
+    grp = kmc.VGroup(world, dims, cell, kind=kind, seed=33, replicas=2, **params)
+    lat = (si.bernoulli_lattice(one.local_shape, 0.5, seed=2) if kind != "zgb"
+           else si.categorical_lattice(one.local_shape, [0.5, 0.25, 0.25], seed=2))
+    one.set_config(lat)
+    grp.set_config(lat)
+    for _ in range(3):
+        one.run(2 * dt, dt, scheme)
+        grp.run(2 * dt, dt, scheme)
+        assert np.array_equal(one.get_config(), grp.get_config())
+    a, b = one.observables(), grp.observables()
+    assert a["events"] == b["events"] > 0
+    for key in ("n_state", "nn_pairs", "n_state_by_colour"):
+        assert np.array_equal(a[key], b[key]), key

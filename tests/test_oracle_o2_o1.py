@@ -95,7 +95,12 @@ def test_o2_scheme_law_1d(scheme):
     lat = bf.Lattice(1, 1, N, 1, q, 2)
     Q, Qc, S = bf.generators(bf_model("adsdes", p), lat)
     start = np.array([1 if lat.colour(i) == 1 else 0 for i in range(N)], np.uint8)
-    law = bf.law(bf.point_mass(S, N, start), Q, Qc, scheme, dt, T, 2)
+    if scheme == "random":   # the realised schedule is shared by all replicas (R4)
+        from oracle.fskmc import substeps, RANDOM
+        seq = [cd for w in range(0, int(round(T / dt)) * 2, 2) for cd in substeps(RANDOM, 2, dt, 21, w)]
+        law = bf.law_sequence(bf.point_mass(S, N, start), Qc, seq)
+    else:
+        law = bf.law(bf.point_mass(S, N, start), Q, Qc, scheme, dt, T, 2)
     cov = bf.coverage_values(lat, S)
     m, v = law @ cov, law @ cov ** 2 - (law @ cov) ** 2
     sim = FSKMC(1, (N,), (q,), "adsdes", model_params(**p), colours=2, replicas=R, seed=21)
