@@ -686,7 +686,10 @@ kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, i
     for (int r = 0; r < world; ++r) out[r] = nullptr;
     for (int r = 0; r < world; ++r) {
         kmc_dist d{};
-        d.rank = r; d.world = world; d.device = device; d.stream = stream; d.nccl_unique_id = nullptr;
+        // ONE stream for the whole group (rank 0 owns it when none is given): the exchange copies of
+        // one rank read another rank's rows, so everything must be ordered on a single stream
+        d.rank = r; d.world = world; d.device = device; d.nccl_unique_id = nullptr;
+        d.stream = (r == 0 || stream) ? stream : (void*)out[0]->stream;
         kmc_status st = create_ctx(geom, model, &d, true, &out[r]);
         if (st != KMC_OK) {
             for (int q = 0; q < r; ++q) { kmc_destroy(out[q]); out[q] = nullptr; }
@@ -739,7 +742,7 @@ kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
     a.C = c->C;
     a.out = c->obs_buf;
     CUDA_TRY(c, launch_observables(a, c->stream));
-    if (c->world > 1)
+    if (c->world > 1 && c->comm)   // NCCL ranks: global sums (virtual ranks return local counts)
         NCCL_TRY(c, g_nccl.AllReduce(c->obs_buf, c->obs_buf, kObsCounters + 1, ncclUint64, ncclSum, c->comm, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_obs, c->obs_buf, (kObsCounters + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
     std::vector<uint32_t> wl;
