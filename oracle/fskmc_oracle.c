@@ -56,45 +56,63 @@ void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint3
 }
 
 /* ------------------------------------------------------------------ */
-/* L0: natural log, the fdlibm e_log.c general-path operation sequence */
-/* (IEEE basic operations only, no contraction).  Domain: [2^-1022, 1]. */
+/* L0: natural log, table-driven, every step one       */
+/* correctly rounded IEEE operation (C99 fma() for the fused steps).    */
+/*   x = 2^e m, m in [sqrt(2)/2, sqrt(2));  j = round(128 m) - 91;      */
+/*   c_j = 128/(j+91), L_j = -log(c_j) (host libm);                      */
+/*   r = fma(m, c_j, -1);  log x = e ln2 + L_j + log1p(r),               */
+/*   log1p(r) = r + r^2 q(r), q the Taylor polynomial to r^7 (Horner).   */
+/* Domain: normal x in (0, 1] (the clock only needs [2^-53, 1]).         */
 /* ------------------------------------------------------------------ */
 static const double ln2_hi = 0x1.62e42feep-1;          /* 3fe62e42 fee00000 */
 static const double ln2_lo = 0x1.a39ef35793c76p-33;    /* 3dea39ef 35793c76 */
-static const double Lg1 = 0x1.5555555555593p-1;        /* 3fe55555 55555593 */
-static const double Lg2 = 0x1.999999997fa04p-2;        /* 3fd99999 9997fa04 */
-static const double Lg3 = 0x1.2492494229359p-2;        /* 3fd24924 94229359 */
-static const double Lg4 = 0x1.c71c51d8e78afp-3;        /* 3fcc71c5 1d8e78af */
-static const double Lg5 = 0x1.7466496cb03dep-3;        /* 3fc74664 96cb03de */
-static const double Lg6 = 0x1.39a09d078c69fp-3;        /* 3fc39a09 d078c69f */
-static const double Lg7 = 0x1.2f112df3e5244p-3;        /* 3fc2f112 df3e5244 */
+#define LOG_TAB_N 91
+static double log_ctab[LOG_TAB_N], log_ltab[LOG_TAB_N];
+static int log_tab_ready = 0;
 
 static inline uint64_t dbits(double x) { uint64_t u; memcpy(&u, &x, 8); return u; }
 static inline double bitsd(uint64_t u) { double x; memcpy(&x, &u, 8); return x; }
 
+static void log_tables(void)
+{
+    for (int j = 0; j < LOG_TAB_N; ++j) {
+        log_ctab[j] = 128.0 / (double)(j + 91);
+        log_ltab[j] = -log(log_ctab[j]);
+    }
+    log_tab_ready = 1;
+}
+
 double orc_log(double x)
 {
-    /* the fdlibm e_log.c reduction and polynomial, evaluated with its single
-     * general formula for every x in the domain (no special-case branches). */
-    uint64_t u = dbits(x);
-    int32_t hx = (int32_t)(u >> 32);
+    if (!log_tab_ready) log_tables();
     if (x == 0.0) return -INFINITY;
-    if (hx < 0x00100000 || hx >= 0x7ff00000) return NAN;   /* outside the specified domain */
-    int32_t k = (hx >> 20) - 1023;
-    hx &= 0x000fffff;
-    int32_t i = (hx + 0x95f64) & 0x100000;
-    u = ((uint64_t)(uint32_t)(hx | (i ^ 0x3ff00000)) << 32) | (u & 0xffffffffu);
-    x = bitsd(u);                             /* x or x/2 normalised to [sqrt(2)/2, sqrt(2)) */
-    k += (i >> 20);
-    double f = x - 1.0;
-    double dk = (double)k;
-    double s = f / (2.0 + f);
-    double z = s * s;
-    double w = z * z;
-    double t1 = w * (Lg2 + w * (Lg4 + w * Lg6));
-    double t2 = z * (Lg1 + w * (Lg3 + w * (Lg5 + w * Lg7)));
-    double R = t2 + t1;
-    return dk * ln2_hi - ((s * (f - R) - dk * ln2_lo) - f);
+    uint64_t u = dbits(x);
+    int e0 = (int)((u >> 52) & 0x7ff) - 1023;
+    if (e0 == -1023 || e0 == 1024 || (u >> 63)) return NAN;      /* outside the specified domain */
+    uint64_t mant = u & 0xFFFFFFFFFFFFFull;
+    int e, idx;
+    double m;
+    if (mant >= 0x6A09E667F3BCDull) {                             /* 1.mant >= sqrt(2): halve */
+        e = e0 + 1;
+        idx = 64 + (int)((mant + (1ull << 45)) >> 46);
+        m = bitsd(0x3FE0000000000000ull | mant);
+    } else {
+        e = e0;
+        idx = 128 + (int)((mant + (1ull << 44)) >> 45);
+        m = bitsd(0x3FF0000000000000ull | mant);
+    }
+    const int j = idx - 91;
+    const double r = fma(m, log_ctab[j], -1.0);
+    double q = fma(r, 0x1.2492492492492p-3, -0x1.5555555555555p-3);    /* 1/7, -1/6 */
+    q = fma(r, q, 0x1.999999999999ap-3);                                 /* 1/5 */
+    q = fma(r, q, -0.25);
+    q = fma(r, q, 0x1.5555555555555p-2);                                 /* 1/3 */
+    q = fma(r, q, -0.5);
+    const double p = fma(r * r, q, r);
+    const double dk = (double)e;
+    double s = log_ltab[j] + p;
+    s = fma(dk, ln2_lo, s);
+    return fma(dk, ln2_hi, s);
 }
 
 /* ------------------------------------------------------------------ */

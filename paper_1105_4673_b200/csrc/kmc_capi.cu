@@ -290,6 +290,10 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D) {
     a.w_lo = (uint32_t)c->window;
     a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
     for (int i = 0; i < c->nclass; ++i) a.rate[i] = c->crate_u64[i];
+    for (int j = 0; j < kLogTab; ++j) {   // log_spec tables, host libm
+        a.log_c[j] = 128.0 / (double)(j + 91);
+        a.log_l[j] = -std::log(a.log_c[j]);
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         if (c->tev_used == c->tev.size()) {
@@ -516,6 +520,10 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     for (int y = 0; y < qy; ++y) { g.col0 |= 1ull << (y * qx); g.colL |= 1ull << (y * qx + qx - 1); }
     g.row0 = lowmask(qx);
     g.rowL = g.row0 << g.shN;
+    g.notcol0 = g.valid & ~g.col0;
+    g.notcolL = g.valid & ~g.colL;
+    g.notrow0 = g.valid & ~g.row0;
+    g.notrowL = g.valid & ~g.rowL;
     c->H_local = (long long)g.My_local * qy;
     c->rank_up = (int)plan[4];
     c->rank_down = (int)plan[5];

@@ -16,6 +16,7 @@
 namespace kmc {
 
 constexpr int kMaxClass = 32;
+constexpr int kLogTab = 91;          // buckets of the table-driven log
 
 // Slot types, used by the host rate table.
 enum SlotType { T_ADS = 0, T_DES = 1, T_HOP = 2, T_COADS = 3, T_O2ADS = 4, T_RCO = 5, T_RO = 6, T_COHOP = 7 };
@@ -28,6 +29,7 @@ struct Geo {
     long long M_global;              // cells per replica (global)
     int shN;                         // q_x*(q_y-1): bit offset of the last row
     uint64_t valid, col0, colL, row0, rowL;
+    uint64_t notcol0, notcolL, notrow0, notrowL;   // valid & ~(...): kept in the param bank, not registers
 };
 
 struct SubstepArgs {
@@ -43,6 +45,8 @@ struct SubstepArgs {
     uint32_t rk0[10], rk1[10];       // Philox round keys k + i*(W0, W1), i = 0..9 (warp-uniform)
     uint32_t w_lo, w_hi_tag;         // window id (tag EVT = 0 in bits 28..31)
     uint64_t rate[kMaxClass];        // u64 fixed-point class rates (R18)
+    double log_c[kLogTab];           // log_spec tables: c_j = 128/(j+91)
+    double log_l[kLogTab];           //   L_j = -log(c_j), host libm
 };
 
 struct ObsArgs {

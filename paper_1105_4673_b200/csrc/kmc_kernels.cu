@@ -39,31 +39,32 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
     return c;
 }
 
-// natural log on [2^-53, 1] (normal inputs only): the fdlibm e_log.c argument reduction and
-// polynomial with its single general formula (no special-case branches, so a
-// warp never diverges here); every operation an explicit round-to-nearest intrinsic so nvcc
-// cannot contract to FMA.
-__device__ __forceinline__ double log_spec(double x) {
+// natural log on normal x in (0, 1]: x = 2^e m, m in [sqrt(2)/2, sqrt(2)),
+// bucket j = round(128 m) - 91, r = fma(m, c_j, -1), log x = e ln2 + L_j + r + r^2 q(r) with q the
+// Taylor polynomial of log1p to r^7.  Division-free and branch-free; every step one explicit
+// round-to-nearest operation (__fma_rn / __dmul_rn / __dadd_rn) so the bits match the CPU oracle.
+// ctab / ltab: the kLogTab-entry tables staged in shared memory.
+__device__ __forceinline__ double log_spec(double x, const double* ctab, const double* ltab) {
     const double ln2_hi = 0x1.62e42feep-1, ln2_lo = 0x1.a39ef35793c76p-33;
-    const double Lg1 = 0x1.5555555555593p-1, Lg2 = 0x1.999999997fa04p-2, Lg3 = 0x1.2492494229359p-2;
-    const double Lg4 = 0x1.c71c51d8e78afp-3, Lg5 = 0x1.7466496cb03dep-3, Lg6 = 0x1.39a09d078c69fp-3;
-    const double Lg7 = 0x1.2f112df3e5244p-3;
-    int hx = __double2hiint(x);
-    const int lx = __double2loint(x);
-    int k = (hx >> 20) - 1023;
-    hx &= 0x000fffff;
-    const int i = (hx + 0x95f64) & 0x100000;
-    const double xn = __hiloint2double(hx | (i ^ 0x3ff00000), lx);
-    k += (i >> 20);
-    const double f = __dsub_rn(xn, 1.0);
-    const double dk = (double)k;
-    const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
-    const double z = __dmul_rn(s, s);
-    const double w = __dmul_rn(z, z);
-    const double t1 = __dmul_rn(w, __dadd_rn(Lg2, __dmul_rn(w, __dadd_rn(Lg4, __dmul_rn(w, Lg6)))));
-    const double t2 = __dmul_rn(z, __dadd_rn(Lg1, __dmul_rn(w, __dadd_rn(Lg3, __dmul_rn(w, __dadd_rn(Lg5, __dmul_rn(w, Lg7)))))));
-    const double R = __dadd_rn(t2, t1);
-    return __dsub_rn(__dmul_rn(dk, ln2_hi), __dsub_rn(__dsub_rn(__dmul_rn(s, __dsub_rn(f, R)), __dmul_rn(dk, ln2_lo)), f));
+    const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+    const int e0 = (int)((u >> 52) & 0x7ff) - 1023;
+    const unsigned long long mant = u & 0xFFFFFFFFFFFFFull;
+    const bool hi = mant >= 0x6A09E667F3BCDull;                   // 1.mant >= sqrt(2): halve
+    const int e = e0 + (hi ? 1 : 0);
+    const int idx = hi ? 64 + (int)((mant + (1ull << 45)) >> 46) : 128 + (int)((mant + (1ull << 44)) >> 45);
+    const double m = __longlong_as_double((long long)((hi ? 0x3FE0000000000000ull : 0x3FF0000000000000ull) | mant));
+    const int j = idx - 91;
+    const double r = __fma_rn(m, ctab[j], -1.0);
+    double q = __fma_rn(r, 0x1.2492492492492p-3, -0x1.5555555555555p-3);
+    q = __fma_rn(r, q, 0x1.999999999999ap-3);
+    q = __fma_rn(r, q, -0.25);
+    q = __fma_rn(r, q, 0x1.5555555555555p-2);
+    q = __fma_rn(r, q, -0.5);
+    const double p = __fma_rn(__dmul_rn(r, r), q, r);
+    const double dk = (double)e;
+    double s = __dadd_rn(ltab[j], p);
+    s = __fma_rn(dk, ln2_lo, s);
+    return __fma_rn(dk, ln2_hi, s);
 }
 
 // position of the k-th (0-based) set bit of a 64-bit word (k < popc(m))
@@ -239,21 +240,25 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     return L;
 }
 
-template <int KIND, int NDIM, int MINB>
-__global__ void __launch_bounds__(256, MINB)
+template <int KIND, int NDIM, int BS, int MINB>
+__global__ void __launch_bounds__(BS, MINB)
 substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
     using M = Model<KIND, NDIM>;
     constexpr int NP = M::NP, NC = M::NC;
     const Geo& g = a.g;
     const unsigned FULL = 0xffffffffu;
+    // log_spec tables -> shared memory (lanes index them by their own bucket)
+    __shared__ double s_logc[kLogTab], s_logl[kLogTab];
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) { s_logc[i] = a.log_c[i]; s_logl[i] = a.log_l[i]; }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long cbeg64 = (unsigned long long)warp * chunk;
     if (cbeg64 >= nactive) return;                                  // warp-uniform
     const uint32_t cbeg = (uint32_t)cbeg64;
     const uint32_t cend = (uint32_t)min(cbeg64 + chunk, (unsigned long long)nactive);
-    const uint64_t notcol0 = g.valid & ~g.col0, notcolL = g.valid & ~g.colL;
-    const uint64_t notrow0 = g.valid & ~g.row0, notrowL = g.valid & ~g.rowL;
+    const uint64_t notcol0 = g.notcol0, notcolL = g.notcolL;
+    const uint64_t notrow0 = g.notrow0, notrowL = g.notrowL;
     uint64_t* planes[2] = {a.plane0, a.plane1};
 
     uint32_t next = cbeg + 32;                                      // warp-uniform queue head
@@ -326,7 +331,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
             }
             const uint64_t j53 = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
             const double U = __dmul_rn(__ull2double_rn(j53 + 1ull), 0x1p-53);
-            const double E = -log_spec(U);
+            const double E = -log_spec(U, s_logc, s_logl);
 
             // a4/a5: class masks, counts and lambda (eq.(totalrate), exact u64)
             uint64_t nb[NP][4];
@@ -418,18 +423,26 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
 template <int KIND, int NDIM>
 static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
     if (nactive <= 0) return cudaSuccess;
-    const int bs = 256;
+    // launch shape (block size, min blocks per SM): env KMC_LB selects an experiment variant
+    static const int lb = [] { const char* e = getenv("KMC_LB"); return e ? atoi(e) : 0; }();
+    int bs = 256;
+    if (KIND == 0 && (lb == 1 || lb == 2)) bs = 128;
     // cells per warp: 32 lanes x a few cells each, so a lane's tail idles for ~1/cpl of the window
     long long cpl = 8;
     while (cpl > 1 && (nactive + 32 * cpl - 1) / (32 * cpl) < 4 * 148 * 8) cpl >>= 1;   // keep >= ~4 waves
     const long long chunk = 32 * cpl;
     const long long nwarps = (nactive + chunk - 1) / chunk;
-    const long long nb = (nwarps * 32 + bs - 1) / bs;
-    static const int minb_env = [] { const char* e = getenv("KMC_MINB"); return e ? atoi(e) : 0; }();
-    if (KIND == 0 && minb_env != 2)
-        substep_kernel<KIND, NDIM, 3><<<(unsigned)nb, bs, 0, s>>>(a, (uint32_t)nactive, (uint32_t)chunk);
-    else
-        substep_kernel<KIND, NDIM, 2><<<(unsigned)nb, bs, 0, s>>>(a, (uint32_t)nactive, (uint32_t)chunk);
+    const unsigned nb = (unsigned)((nwarps * 32 + bs - 1) / bs);
+    const uint32_t na = (uint32_t)nactive, ch = (uint32_t)chunk;
+    if constexpr (KIND == 0) {
+        // spin flip default: <= 80 registers, 3 blocks of 256 (24 warps) per SM
+        if (lb == 1) substep_kernel<KIND, NDIM, 128, 5><<<nb, 128, 0, s>>>(a, na, ch);        // <= 96 regs, 20 warps
+        else if (lb == 2) substep_kernel<KIND, NDIM, 128, 4><<<nb, 128, 0, s>>>(a, na, ch);   // <= 128 regs, 16 warps
+        else if (lb == 3) substep_kernel<KIND, NDIM, 256, 2><<<nb, 256, 0, s>>>(a, na, ch);   // <= 128 regs, 16 warps
+        else substep_kernel<KIND, NDIM, 256, 3><<<nb, 256, 0, s>>>(a, na, ch);
+    } else {
+        substep_kernel<KIND, NDIM, 256, 2><<<nb, 256, 0, s>>>(a, na, ch);
+    }
     return cudaGetLastError();
 }
 
