@@ -281,6 +281,8 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D) {
     a.C = c->C;
     a.D = D;
     a.inv_scale = std::ldexp(1.0, -c->F);
+    a.inv_half = 1.0 / (double)(c->g.Mx / 2);
+    a.inv_R = 1.0 / (double)c->g.R;
     a.key0 = (uint32_t)c->geom.seed;
     a.key1 = (uint32_t)(c->geom.seed >> 32);
     for (int i = 0; i < 10; ++i) {
@@ -294,6 +296,12 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D) {
         a.log_c[j] = 128.0 / (double)(j + 91);
         a.log_l[j] = -std::log(a.log_c[j]);
     }
+    a.lcoef[0] = 0x1.2492492492492p-3;      // 1/7
+    a.lcoef[1] = -0x1.5555555555555p-3;     // -1/6
+    a.lcoef[2] = 0x1.999999999999ap-3;      // 1/5
+    a.lcoef[3] = 0x1.5555555555555p-2;      // 1/3
+    a.lcoef[4] = 0x1.62e42feep-1;           // ln2_hi (fdlibm)
+    a.lcoef[5] = 0x1.a39ef35793c76p-33;     // ln2_lo (fdlibm)
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         if (c->tev_used == c->tev.size()) {

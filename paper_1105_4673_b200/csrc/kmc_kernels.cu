@@ -44,8 +44,10 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 // Taylor polynomial of log1p to r^7.  Division-free and branch-free; every step one explicit
 // round-to-nearest operation (__fma_rn / __dmul_rn / __dadd_rn) so the bits match the CPU oracle.
 // ctab / ltab: the kLogTab-entry tables staged in shared memory.
-__device__ __forceinline__ double log_spec(double x, const double* ctab, const double* ltab) {
-    const double ln2_hi = 0x1.62e42feep-1, ln2_lo = 0x1.a39ef35793c76p-33;
+__device__ __forceinline__ double log_spec(double x, const double* ctab, const double* ltab, const double* lc) {
+    // lc = {1/7, -1/6, 1/5, 1/3, ln2_hi, ln2_lo} from the kernel parameters (constant bank operands:
+    // full 64-bit FP64 constants would otherwise be rebuilt with uniform moves every event)
+    const double ln2_hi = lc[4], ln2_lo = lc[5];
     const unsigned long long u = (unsigned long long)__double_as_longlong(x);
     const int e0 = (int)((u >> 52) & 0x7ff) - 1023;
     const unsigned long long mant = u & 0xFFFFFFFFFFFFFull;
@@ -55,16 +57,25 @@ __device__ __forceinline__ double log_spec(double x, const double* ctab, const d
     const double m = __longlong_as_double((long long)((hi ? 0x3FE0000000000000ull : 0x3FF0000000000000ull) | mant));
     const int j = idx - 91;
     const double r = __fma_rn(m, ctab[j], -1.0);
-    double q = __fma_rn(r, 0x1.2492492492492p-3, -0x1.5555555555555p-3);
-    q = __fma_rn(r, q, 0x1.999999999999ap-3);
+    double q = __fma_rn(r, lc[0], lc[1]);
+    q = __fma_rn(r, q, lc[2]);
     q = __fma_rn(r, q, -0.25);
-    q = __fma_rn(r, q, 0x1.5555555555555p-2);
+    q = __fma_rn(r, q, lc[3]);
     q = __fma_rn(r, q, -0.5);
     const double p = __fma_rn(__dmul_rn(r, r), q, r);
     const double dk = (double)e;
     double s = __dadd_rn(ltab[j], p);
     s = __fma_rn(dk, ln2_lo, s);
     return __fma_rn(dk, ln2_hi, s);
+}
+
+// q = n / d, rem = n % d for n < 2^32 via the FP64 reciprocal inv = RN(1/d): n*inv is within
+// 2^-52 relative of n/d, so floor(n*inv) is floor(n/d) or, when n/d is an integer, possibly one
+// less -- fixed by one compare.  ~7 instructions instead of a ~40-instruction integer division.
+__device__ __forceinline__ void fast_divmod(uint32_t n, uint32_t d, double inv, uint32_t& q, uint32_t& rem) {
+    q = __double2uint_rz(__dmul_rn(__uint2double_rn(n), inv));
+    rem = n - q * d;
+    if (rem >= d) { ++q; rem -= d; }
 }
 
 // position of the k-th (0-based) set bit of a 64-bit word (k < popc(m))
@@ -201,10 +212,10 @@ template <int NDIM>
 __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     const Geo& g = a.g;
     const uint32_t half = (uint32_t)g.Mx >> 1;
-    const uint32_t j = t % half;
-    const uint32_t rest = t / half;
-    const uint32_t r = rest % (uint32_t)g.R;
-    const uint32_t rowsel = rest / (uint32_t)g.R;
+    uint32_t rest, j, rowsel, r;
+    fast_divmod(t, half, a.inv_half, rest, j);
+    if (g.R == 1) { rowsel = rest; r = 0; }
+    else fast_divmod(rest, (uint32_t)g.R, a.inv_R, rowsel, r);
     uint32_t cy, cx;
     if (NDIM == 1) {
         cy = 0;
@@ -318,93 +329,88 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     };
 
     if (have) load(ci);
-    while (__any_sync(FULL, have)) {
-        bool fin = false;
-        if (have) {
-            // RNG and -ln U first: independent of lambda, so they overlap the mask chain (ILP)
-            uint4 x = make_uint4(k, gid32, a.w_lo, a.w_hi_tag);
+    // The event step is one branch-free basic block: lanes without a cell (queue exhausted) and
+    // lanes whose window ended compute it too, with the update masked off (ab = 0), so the warp
+    // never diverges inside the step and the scheduler can interleave its independent chains.
+    for (;;) {
+        // RNG and -ln U first: independent of lambda, so they overlap the mask chain (ILP)
+        uint4 x = make_uint4(k, gid32, a.w_lo, a.w_hi_tag);
 #pragma unroll
-            for (int rd = 0; rd < 10; ++rd) {
-                const uint32_t lo0 = 0xD2511F53u * x.x, hi0 = __umulhi(0xD2511F53u, x.x);
-                const uint32_t lo1 = 0xCD9E8D57u * x.z, hi1 = __umulhi(0xCD9E8D57u, x.z);
-                x = make_uint4(hi1 ^ x.y ^ a.rk0[rd], lo1, hi0 ^ x.w ^ a.rk1[rd], lo0);
-            }
-            const uint64_t j53 = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
-            const double U = __dmul_rn(__ull2double_rn(j53 + 1ull), 0x1p-53);
-            const double E = -log_spec(U, s_logc, s_logl);
+        for (int rd = 0; rd < 10; ++rd) {
+            const uint32_t lo0 = 0xD2511F53u * x.x, hi0 = __umulhi(0xD2511F53u, x.x);
+            const uint32_t lo1 = 0xCD9E8D57u * x.z, hi1 = __umulhi(0xCD9E8D57u, x.z);
+            x = make_uint4(hi1 ^ x.y ^ a.rk0[rd], lo1, hi0 ^ x.w ^ a.rk1[rd], lo0);
+        }
+        const uint64_t j53 = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
+        const double U = __dmul_rn(__ull2double_rn(j53 + 1ull), 0x1p-53);
+        const double E = -log_spec(U, s_logc, s_logl, a.lcoef);
 
-            // a4/a5: class masks, counts and lambda (eq.(totalrate), exact u64)
-            uint64_t nb[NP][4];
+        // a4/a5: class masks, counts and lambda (eq.(totalrate), exact u64)
+        uint64_t nb[NP][4];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                nb[p][0] = ((P[p] << 1) & notcol0) | h[p][0];
-                nb[p][1] = ((P[p] >> 1) & notcolL) | h[p][1];
-                if (NDIM == 2) {
-                    nb[p][2] = ((P[p] << g.qx) & g.valid) | h[p][2];
-                    nb[p][3] = (P[p] >> g.qx) | h[p][3];
-                } else {
-                    nb[p][2] = nb[p][3] = 0;
-                }
-            }
-            uint64_t m[NC];
-            M::masks(P, nb, g.valid, m);
-            uint32_t cnt[NC];
-            uint64_t lam = 0;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                cnt[c] = __popcll(m[c]);
-                lam += (uint64_t)cnt[c] * a.rate[c];
-            }
-            const double lamd = __dmul_rn(__ull2double_rn(lam), a.inv_scale);
-            const double tau = __ddiv_rn(E, lamd);
-            const double tn = __dadd_rn(tclock, tau);
-            if (lam == 0 || tn >= a.D) {                           // quiescent, or R5 (pending event discarded)
-                fin = true;
+        for (int p = 0; p < NP; ++p) {
+            nb[p][0] = ((P[p] << 1) & notcol0) | h[p][0];
+            nb[p][1] = ((P[p] >> 1) & notcolL) | h[p][1];
+            if (NDIM == 2) {
+                nb[p][2] = ((P[p] << g.qx) & g.valid) | h[p][2];
+                nb[p][3] = (P[p] >> g.qx) | h[p][3];
             } else {
-                tclock = tn;
-                // eq.(skeleton): class = smallest c with prefix(c) > r, r = floor(x2 lambda / 2^32)
-                const uint64_t rr = (uint64_t)x.z * (lam >> 32) + (uint64_t)__umulhi(x.z, (uint32_t)lam);
-                uint64_t cum = 0, selm = m[NC - 1];
-                uint32_t selc = cnt[NC - 1];
-                int seld = M::desc(NC - 1);
-                bool found = false;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    cum += (uint64_t)cnt[c] * a.rate[c];
-                    const bool hit = !found && cum > rr;
-                    if (hit) { selm = m[c]; selc = cnt[c]; seld = M::desc(c); }
-                    found = found || hit;
-                }
-                // site: the kk-th member of the class in row-major order, kk = floor(x3 cnt / 2^32)
-                const int s = select_bit64(selm, __umulhi(x.w, selc));
-                const uint64_t ab = 1ull << s;
-                if (seld & D_A0) P[0] ^= ab;
-                if (NP > 1 && (seld & D_A1)) P[NP - 1] ^= ab;
-                if (seld & D_HASP) {
-                    const int d = (seld >> 4) & 3;
-                    uint64_t inner, pb;
-                    if (d == 0)      { inner = notcol0; pb = ab >> 1; }
-                    else if (d == 1) { inner = notcolL; pb = ab << 1; }
-                    else if (d == 2) { inner = notrow0; pb = ab >> g.qx; }
-                    else             { inner = notrowL; pb = ab << g.qx; }
-                    const bool in_cell = (ab & inner) != 0;
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        if (seld & (D_P0 << p)) {
-                            if (in_cell) P[p] ^= pb;
-                            else {
-#pragma unroll
-                                for (int dd = 0; dd < 4; ++dd)
-                                    if (dd == d) h[p][dd] ^= ab;
-                            }
-                        }
-                    }
-                }
-                ++k;
+                nb[p][2] = nb[p][3] = 0;
             }
         }
+        uint64_t m[NC];
+        M::masks(P, nb, g.valid, m);
+        uint32_t cnt[NC];
+        uint64_t lam = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            cnt[c] = __popcll(m[c]);
+            lam += (uint64_t)cnt[c] * a.rate[c];
+        }
+        const double lamd = __dmul_rn(__ull2double_rn(lam), a.inv_scale);
+        const double tau = __ddiv_rn(E, lamd);
+        const double tn = __dadd_rn(tclock, tau);
+        // accept unless quiescent (lambda = 0) or past the window end (R5: pending event discarded)
+        const bool accept = have && lam != 0 && tn < a.D;
+        const bool fin = have && !accept;
+        tclock = accept ? tn : tclock;
+        // eq.(skeleton): class = smallest c with prefix(c) > r, r = floor(x2 lambda / 2^32)
+        const uint64_t rr = (uint64_t)x.z * (lam >> 32) + (uint64_t)__umulhi(x.z, (uint32_t)lam);
+        uint64_t cum = 0, selm = m[NC - 1];
+        uint32_t selc = cnt[NC - 1];
+        int seld = M::desc(NC - 1);
+        bool found = false;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            cum += (uint64_t)cnt[c] * a.rate[c];
+            const bool hit = !found && cum > rr;
+            selm = hit ? m[c] : selm;
+            selc = hit ? cnt[c] : selc;
+            seld = hit ? M::desc(c) : seld;
+            found = found || hit;
+        }
+        // site: the kk-th member of the class in row-major order, kk = floor(x3 cnt / 2^32)
+        const int s = select_bit64(selm, __umulhi(x.w, selc));
+        const uint64_t ab = accept ? (1ull << s) : 0ull;
+        if (seld & D_A0) P[0] ^= ab;
+        if (NP > 1 && (seld & D_A1)) P[NP - 1] ^= ab;
+        if (seld & D_HASP) {
+            const int d = (seld >> 4) & 3;
+            const uint64_t inner = d == 0 ? notcol0 : d == 1 ? notcolL : d == 2 ? notrow0 : notrowL;
+            const uint64_t pb = d == 0 ? ab >> 1 : d == 1 ? ab << 1 : d == 2 ? ab >> g.qx : ab << g.qx;
+            const bool in_cell = (ab & inner) != 0;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const bool tog = (seld & (D_P0 << p)) != 0;
+                P[p] ^= (tog && in_cell) ? pb : 0ull;
+#pragma unroll
+                for (int dd = 0; dd < 4; ++dd) h[p][dd] ^= (tog && !in_cell && dd == d) ? ab : 0ull;
+            }
+        }
+        k += accept ? 1u : 0u;
+
         const unsigned fm = __ballot_sync(FULL, fin);
-        if (fm) {
+        if (fm) {                                                  // warp-uniform
             if (fin) {
                 store(ci);
                 ci = next + __popc(fm & ((1u << lane) - 1u));
@@ -412,6 +418,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
                 if (have) load(ci);
             }
             next += __popc(fm);
+            if (!__any_sync(FULL, have)) break;
         }
     }
     // event total: warp-aggregated
