@@ -109,6 +109,8 @@ struct kmc_ctx {
     uint64_t* ghost_snap = nullptr;          // [2 rows][nplanes] snapshot / delta buffers (world > 1)
     uint64_t* ghost_recv = nullptr;
     unsigned long long* h_obs = nullptr;     // pinned
+    unsigned int* h_err = nullptr;           // pinned (set_config validation flag)
+    uint64_t* spare[2] = {nullptr, nullptr}; // set_config double buffer
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
@@ -564,6 +566,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
         ok = ok && alloc((void**)&c->ghost_recv, (size_t)4 * g.R * g.Mx * 8);
     }
     ok = ok && cudaMallocHost((void**)&c->h_obs, (kObsCounters + 1) * 8) == cudaSuccess;
+    ok = ok && cudaMallocHost((void**)&c->h_err, 4) == cudaSuccess;
     if (!ok) { kmc_destroy(c); return fail(nullptr, KMC_ENOMEM, "device allocation failed (%lld words)", c->plane_words); }
     for (int p = 0; p < c->nplanes; ++p) cudaMemsetAsync(c->planes[p], 0, (size_t)c->plane_words * 8, c->stream);
     cudaMemsetAsync(c->wev, 0, (size_t)owned * 4, c->stream);
@@ -595,7 +598,9 @@ void kmc_destroy(kmc_ctx* c) {
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
     cudaFree(c->wev); cudaFree(c->ev_total); cudaFree(c->obs_buf); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv);
+    cudaFree(c->spare[0]); cudaFree(c->spare[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);
+    if (c->h_err) cudaFreeHost(c->h_err);
     for (auto& pr : c->tev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -645,17 +650,18 @@ kmc_status kmc_set_config(kmc_ctx* c, const uint8_t* host, int64_t nbytes) {
     // validate in a scratch copy of the planes so an invalid slab leaves the lattice unchanged
     CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->staging, host, (size_t)nbytes, cudaMemcpyHostToDevice, c->stream));
-    uint64_t* tmp[2] = {nullptr, nullptr};
-    for (int p = 0; p < c->nplanes; ++p) CUDA_TRY(c, cudaMallocAsync((void**)&tmp[p], (size_t)c->plane_words * 8, c->stream));
-    CUDA_TRY(c, launch_pack(c->g, c->staging, tmp[0], tmp[1], c->nstates, c->err_flag, c->stream));
-    unsigned bad = 0;
-    CUDA_TRY(c, cudaMemcpyAsync(&bad, c->err_flag, 4, cudaMemcpyDeviceToHost, c->stream));
+    // persistent spare planes (allocated once): pack there, swap in only if every spin was valid
+    for (int p = 0; p < c->nplanes; ++p)
+        if (!c->spare[p] && cudaMalloc((void**)&c->spare[p], (size_t)c->plane_words * 8) != cudaSuccess)
+            return fail(c, KMC_ENOMEM, "spare plane allocation failed");
+    if (c->g.ghost)   // ghost rows are refreshed by the next exchange; keep them defined
+        for (int p = 0; p < c->nplanes; ++p)
+            CUDA_TRY(c, cudaMemcpyAsync(c->spare[p], c->planes[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(c, launch_pack(c->g, c->staging, c->spare[0], c->spare[1], c->nstates, c->err_flag, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->err_flag, 4, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    if (!bad)
-        for (int p = 0; p < c->nplanes; ++p) std::swap(tmp[p], c->planes[p]);
-    for (int p = 0; p < c->nplanes; ++p) CUDA_TRY(c, cudaFreeAsync(tmp[p], c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    if (bad) return fail(c, KMC_EINVAL, "spin value >= %d in the configuration", c->nstates);
+    if (*c->h_err) return fail(c, KMC_EINVAL, "spin value >= %d in the configuration", c->nstates);
+    for (int p = 0; p < c->nplanes; ++p) std::swap(c->spare[p], c->planes[p]);
     return KMC_OK;
 }
 
