@@ -148,6 +148,15 @@ kmc_status kmc_set_state(kmc_ctx* ctx, uint64_t windows, double time);
 kmc_status kmc_rate_table(const kmc_ctx* ctx, int32_t* n, int32_t* type, int32_t* dir, int32_t* kappa,
                           double* rate, uint64_t* rate_u64, int32_t* F);
 
+/* Window-kernel choice (performance only; results are bit-identical):
+ *   KMC_KERNEL_QUEUE: lane-per-cell kernel, per-warp cell queues, closure loaded from global memory;
+ *   KMC_KERNEL_TILE:  2D spin-flip only -- a CTA stages a 32x64-cell tile + halo in shared memory and
+ *                     runs its active cells from a CTA queue (best when a window holds few events);
+ *   KMC_KERNEL_AUTO:  tile when D x sites x mean class rate < 16, else queue (env KMC_TILE=0/1 overrides).
+ * KMC_EINVAL for an unknown mode. */
+typedef enum { KMC_KERNEL_AUTO = 0, KMC_KERNEL_QUEUE = 1, KMC_KERNEL_TILE = 2 } kmc_kernel_mode;
+kmc_status kmc_set_kernel(kmc_ctx* ctx, int32_t mode);
+
 /* Kernel timing (bench): when enabled, every sub-step kernel is bracketed by CUDA events on the
  * launching stream; kmc_timing returns the summed kernel milliseconds and launch count since the
  * last reset (synchronises). */

@@ -27,7 +27,9 @@ EXPORTS = [
     "kmc_run", "kmc_substep", "kmc_observables", "kmc_get_state", "kmc_set_state",
     "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
     "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
+    "kmc_set_kernel",
 ]
+KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
 
 class KmcModel(ctypes.Structure):
@@ -96,6 +98,7 @@ def lib():
         "kmc_vgroup_create": ([P(KmcGeometry), P(KmcModel), i32, i32, vp, vp], i32),
         "kmc_vgroup_run": ([vp, i32, dbl, dbl, i32], i32),
         "kmc_vgroup_sync": ([vp, i32], i32),
+        "kmc_set_kernel": ([vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -258,6 +261,11 @@ class KMC:
         k = n.value
         return {"n": k, "type": np.array(ty[:k]), "dir": np.array(di[:k]), "kappa": np.array(ka[:k]),
                 "rate": np.array(ra[:k]), "rate_u64": np.array(ru[:k], dtype=np.uint64), "F": F.value}
+
+    def set_kernel(self, mode="auto"):
+        """Window-kernel choice: 'auto', 'queue' (lane-per-cell, global closure loads) or 'tile'
+        (2D spin flip: shared-memory tiles).  Performance only; results are bit-identical."""
+        self._check(self._L.kmc_set_kernel(self._ctx, KERNELS[mode] if isinstance(mode, str) else int(mode)))
 
     # ---- timing (bench) --------------------------------------------------------
     def enable_timing(self, on=True):

@@ -114,6 +114,8 @@ struct kmc_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
+    double tile_rate_bound = 0.0;            // rough events per unit time per cell (kernel choice)
+    int kernel_mode = 0;                     // kmc_set_kernel
     // schedule state
     uint64_t window = 0;
     double time = 0.0;
@@ -317,7 +319,16 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D) {
         ++c->tev_used;
         CUDA_TRY(c, cudaEventRecord(e0, c->stream));
     }
-    CUDA_TRY(c, launch_substep(c->kind, a, active_cells(c), c->stream));
+    // kernel choice: the shared-memory tile kernel for 2D spin-flip windows (KMC_TILE=0 forces the
+    // lane-queue kernel, KMC_TILE=1 the tile kernel); both give bit-identical results
+    static const int tile_env = [] { const char* e = getenv("KMC_TILE"); return e ? atoi(e) : -1; }();
+    int mode = c->kernel_mode;                                   // kmc_set_kernel: 0 auto, 1 queue, 2 tile
+    if (mode == KMC_KERNEL_AUTO && tile_env >= 0) mode = tile_env ? KMC_KERNEL_TILE : KMC_KERNEL_QUEUE;
+    bool use_tile = c->kind == KMC_ADSDES && c->g.ndim == 2 && mode != KMC_KERNEL_QUEUE;
+    if (use_tile && mode == KMC_KERNEL_AUTO) use_tile = D * c->tile_rate_bound < 16.0;   // few events per cell
+    cudaError_t le = use_tile ? launch_substep_tile(a, c->stream) : cudaErrorNotSupported;
+    if (le == cudaErrorNotSupported) le = launch_substep(c->kind, a, active_cells(c), c->stream);
+    CUDA_TRY(c, le);
     if (c->timing) CUDA_TRY(c, cudaEventRecord(e1, c->stream));
     c->window += 1;
     return KMC_OK;
@@ -542,6 +553,11 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     c->nclass = build_classes(*model, ndim, c->ctype, c->cdir, c->ckappa, c->crate);
     c->F = quantise(c->crate, c->nclass, (long long)g.nsite * types_per_site(c->kind, 2 * ndim), c->crate_u64);
     if (c->F < 0) { delete c; return fail(nullptr, KMC_EINVAL, "rates must be finite and >= 0 (and quantisable)"); }
+    {   // kernel-choice heuristic: sites x mean class rate ~ events per unit time per cell
+        double s = 0.0;
+        for (int i = 0; i < c->nclass; ++i) s += c->crate[i];
+        c->tile_rate_bound = (double)g.nsite * s / (double)c->nclass;
+    }
 
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) { delete c; return fail(nullptr, KMC_ECUDA, "cudaSetDevice(%d): %s", dist ? dist->device : 0, cudaGetErrorString(e)); }
@@ -826,6 +842,13 @@ kmc_status kmc_rate_table(const kmc_ctx* c, int32_t* n, int32_t* type, int32_t* 
         if (rate) rate[i] = c->crate[i];
         if (rate_u64) rate_u64[i] = c->crate_u64[i];
     }
+    return KMC_OK;
+}
+
+kmc_status kmc_set_kernel(kmc_ctx* c, int32_t mode) {
+    if (!c) return KMC_EINVAL;
+    if (mode < KMC_KERNEL_AUTO || mode > KMC_KERNEL_TILE) return fail(c, KMC_EINVAL, "unknown kernel mode %d", mode);
+    c->kernel_mode = mode;
     return KMC_OK;
 }
 

@@ -63,6 +63,7 @@ constexpr int kObsCounters = 4 + 16 + 16;
 
 // kernels.cu
 cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cudaStream_t s);
+cudaError_t launch_substep_tile(const SubstepArgs& a, cudaStream_t s);   // kmc_tile.cu (2D spin flip)
 cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s);
 cudaError_t launch_pack(const Geo& g, const uint8_t* in, uint64_t* p0, uint64_t* p1, int nstates,
                         unsigned int* err, cudaStream_t s);

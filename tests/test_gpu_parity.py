@@ -90,6 +90,28 @@ def test_bit_exact_every_window(name):
     assert orc.events > 0
 
 
+SPIN_FLIP_2D = [n for n, c in CASES.items() if c[0] == 2 and c[3] == "adsdes"]
+SPIN_FLIP_2D_EXTRA = {
+    # 4 colours for a spin-flip model; partial tiles (dims not multiples of the 32x64-cell tile)
+    "2d_ising_4col": (2, (48, 80), (2, 2), "adsdes", dict(ca=1, cd=1, beta=1.3, K=1.0, h=-2.0), 4, 2, 0.5, "strang", 0.5, 2),
+    "2d_ising_big_partial": (2, (328, 544), (4, 4), "adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), 0, 1, 0.5, "lie", 0.05, 3),
+}
+
+
+@pytest.mark.parametrize("kernel", ["queue", "tile"])
+@pytest.mark.parametrize("name", SPIN_FLIP_2D + list(SPIN_FLIP_2D_EXTRA))
+def test_bit_exact_kernel_modes(name, kernel):
+    """Both window kernels (lane-queue and shared-memory tile) are bit-exact vs O2 every window."""
+    ndim, dims, cell, kind, params, C, R, init, scheme, dt, nmacro = {**CASES, **SPIN_FLIP_2D_EXTRA}[name]
+    gpu, orc = make_pair(ndim, dims, cell, kind, params, C, R)
+    gpu.set_kernel(kernel)
+    lat = si.bernoulli_lattice(gpu.local_shape, init, seed=si.SEED_BASE + 4)
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    run_windows(gpu, orc, scheme, dt, nmacro)
+    assert orc.events > 0
+
+
 @pytest.mark.parametrize("scheme", ["lie", "strang", "random"])
 def test_library_schedule_matches_oracle_run(scheme):
     """kmc_run's own schedule (R1-R4, R20 truncation) equals the oracle's run()."""
@@ -238,6 +260,10 @@ def test_virtual_ranks_bit_identical(kind, params, scheme, dt, cell, world):
     dims = (64, 32)
     one = kmc.KMC(2, dims, cell, kind=kind, seed=33, replicas=2, **params)
     grp = kmc.VGroup(world, dims, cell, kind=kind, seed=33, replicas=2, **params)
+    if kind == "adsdes":          # ghost-row slabs through the tile kernel, G = 1 through the queue kernel
+        one.set_kernel("queue")
+        for rk in grp.ranks:
+            rk.set_kernel("tile")
     lat = (si.bernoulli_lattice(one.local_shape, 0.5, seed=2) if kind != "zgb"
            else si.categorical_lattice(one.local_shape, [0.5, 0.25, 0.25], seed=2))
     one.set_config(lat)
