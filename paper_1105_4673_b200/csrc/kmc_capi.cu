@@ -85,6 +85,11 @@ void philox_host(uint32_t c[4], uint32_t k0, uint32_t k1) {
 }
 }  // namespace
 
+struct VgShared {
+    cudaStream_t stream = nullptr;
+    int refs = 0;
+};
+
 struct kmc_ctx {
     kmc_geometry geom{};
     kmc_model model{};
@@ -116,6 +121,7 @@ struct kmc_ctx {
     bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
     double tile_rate_bound = 0.0;            // rough events per unit time per cell (kernel choice)
     int kernel_mode = 0;                     // kmc_set_kernel
+    struct VgShared* vg_shared = nullptr;    // virtual-rank group stream (reference counted)
     // schedule state
     uint64_t window = 0;
     double time = 0.0;
@@ -619,6 +625,11 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto& pr : c->tev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (c->vg_shared && --c->vg_shared->refs == 0) {
+        cudaStreamDestroy(c->vg_shared->stream);
+        delete c->vg_shared;
+    }
+    cudaGetLastError();   // teardown is best effort: do not leave a stale error for the next call
     delete c;
 }
 
@@ -722,17 +733,29 @@ kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, i
     if (!geom || !model || !out || world < 2) return fail(nullptr, KMC_EINVAL, "vgroup needs world >= 2");
     if (geom->ndim != 2) return fail(nullptr, KMC_EINVAL, "vgroup: 2D lattices only (1D shards replicas)");
     for (int r = 0; r < world; ++r) out[r] = nullptr;
+    // ONE stream for the whole group: the exchange copies of one rank read another rank's rows, so
+    // everything must be ordered on a single stream.  If none is given the group creates it and the
+    // last rank destroyed releases it (shared, reference counted).
+    VgShared* sh = nullptr;
+    if (!stream) {
+        if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, KMC_ECUDA, "cudaSetDevice(%d)", device);
+        sh = new VgShared();
+        if (cudaStreamCreateWithFlags(&sh->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete sh;
+            return fail(nullptr, KMC_ECUDA, "cudaStreamCreate failed");
+        }
+        stream = (void*)sh->stream;
+    }
     for (int r = 0; r < world; ++r) {
         kmc_dist d{};
-        // ONE stream for the whole group (rank 0 owns it when none is given): the exchange copies of
-        // one rank read another rank's rows, so everything must be ordered on a single stream
-        d.rank = r; d.world = world; d.device = device; d.nccl_unique_id = nullptr;
-        d.stream = (r == 0 || stream) ? stream : (void*)out[0]->stream;
+        d.rank = r; d.world = world; d.device = device; d.nccl_unique_id = nullptr; d.stream = stream;
         kmc_status st = create_ctx(geom, model, &d, true, &out[r]);
         if (st != KMC_OK) {
             for (int q = 0; q < r; ++q) { kmc_destroy(out[q]); out[q] = nullptr; }
+            if (sh && sh->refs == 0) { cudaStreamDestroy(sh->stream); delete sh; }
             return st;
         }
+        if (sh) { out[r]->vg_shared = sh; ++sh->refs; }
     }
     return KMC_OK;
 }

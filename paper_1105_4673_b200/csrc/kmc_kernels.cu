@@ -150,7 +150,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
                 }
             }
         }
-        a.wev[L.iev] += k;
+        atomicAdd(&a.wev[L.iev], k);   // RED (no return): a plain += would stall on the load
         evsum += k;
     };
 

@@ -93,7 +93,7 @@ tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
                 if (k) {   // a6: write the cell back once, count its events
                     const uint32_t gi = (uint32_t)(y0 + lr + g.ghost) * rowlen + rbase + (uint32_t)(x0 + lc);
                     a.plane0[gi] = P[0];
-                    a.wev[(uint32_t)(y0 + lr) * rowlen + rbase + (uint32_t)(x0 + lc)] += k;
+                    atomicAdd(&a.wev[(uint32_t)(y0 + lr) * rowlen + rbase + (uint32_t)(x0 + lc)], k);   // RED
                     evsum += k;
                 }
                 t = base + __popc(fm & ((1u << lane) - 1u));
