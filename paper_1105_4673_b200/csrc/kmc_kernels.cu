@@ -86,7 +86,7 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     return L;
 }
 
-template <int KIND, int NDIM, int BS, int MINB>
+template <int KIND, int NDIM, int BS, int MINB, bool MH>
 __global__ void __launch_bounds__(BS, MINB)
 substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
     using M = Model<KIND, NDIM>;
@@ -123,7 +123,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         for (int p = 0; p < NP; ++p) {
             const uint64_t* pl = planes[p];
             P[p] = pl[L.iC];
-            halo_from_words(g, pl[L.iW], pl[L.iE], NDIM == 2 ? pl[L.iN] : 0, NDIM == 2 ? pl[L.iS] : 0, h[p], NDIM == 2);
+            halo_from_words<MH>(g, pl[L.iW], pl[L.iE], NDIM == 2 ? pl[L.iN] : 0, NDIM == 2 ? pl[L.iS] : 0, h[p], NDIM == 2);
         }
     };
     // a6: write the cell back once per window (+ halo deltas for hop / pair events)
@@ -138,13 +138,15 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
                 // halo deltas.  Our halo bits of the neighbour words are written by no other cell
                 // in this window (same-colour closures are disjoint, R6), so re-reading them gives
                 // the window-start values; the XOR touches only those bits (order-free).
-                const uint64_t dW = h[p][0] ^ ((pl[L.iW] >> (g.qx - 1)) & g.col0);
-                const uint64_t dE = h[p][1] ^ ((pl[L.iE] << (g.qx - 1)) & g.colL);
+                uint64_t hW, hE, hN, hS;
+                halo_split<MH>(g, h[p], hW, hE, hN, hS);
+                const uint64_t dW = hW ^ ((pl[L.iW] >> (g.qx - 1)) & g.col0);
+                const uint64_t dE = hE ^ ((pl[L.iE] << (g.qx - 1)) & g.colL);
                 if (dW) atomicXor((unsigned long long*)&pl[L.iW], (unsigned long long)(dW << (g.qx - 1)));
                 if (dE) atomicXor((unsigned long long*)&pl[L.iE], (unsigned long long)(dE >> (g.qx - 1)));
                 if (NDIM == 2) {
-                    const uint64_t dN = h[p][2] ^ ((pl[L.iN] >> g.shN) & g.row0);
-                    const uint64_t dS = h[p][3] ^ ((pl[L.iS] << g.shN) & g.rowL);
+                    const uint64_t dN = hN ^ ((pl[L.iN] >> g.shN) & g.row0);
+                    const uint64_t dS = hS ^ ((pl[L.iS] << g.shN) & g.rowL);
                     if (dN) atomicXor((unsigned long long*)&pl[L.iN], (unsigned long long)(dN << g.shN));
                     if (dS) atomicXor((unsigned long long*)&pl[L.iS], (unsigned long long)(dS >> g.shN));
                 }
@@ -159,7 +161,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     // lanes whose window ended compute it too, with the update masked off, so the warp never
     // diverges inside the step and the scheduler can interleave its independent chains.
     for (;;) {
-        const bool fin = event_step<KIND, NDIM>(a, P, h, k, tclock, gid32, have, s_logc, s_logl);
+        const bool fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logc, s_logl);
         const unsigned fm = __ballot_sync(FULL, fin);
         if (fm) {                                                  // warp-uniform
             if (fin) {
@@ -184,7 +186,7 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
     // launch shape (block size, min blocks per SM): env KMC_LB selects an experiment variant
     static const int lb = [] { const char* e = getenv("KMC_LB"); return e ? atoi(e) : 0; }();
     int bs = 256;
-    if (KIND == 0 && (lb == 1 || lb == 2)) bs = 128;
+    if (KIND == 0 && lb == 1 && a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2)) bs = 128;
     // cells per warp: 32 lanes x a few cells each, so a lane's tail idles for ~1/cpl of the window
     long long cpl = 8;
     while (cpl > 1 && (nactive + 32 * cpl - 1) / (32 * cpl) < 4 * 148 * 8) cpl >>= 1;   // keep >= ~4 waves
@@ -192,14 +194,17 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
     const long long nwarps = (nactive + chunk - 1) / chunk;
     const unsigned nb = (unsigned)((nwarps * 32 + bs - 1) / bs);
     const uint32_t na = (uint32_t)nactive, ch = (uint32_t)chunk;
+    // merged halo boards need disjoint first/last columns (and rows in 2D)
+    const bool mh = a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2);
     if constexpr (KIND == 0) {
         // spin flip default: <= 80 registers, 3 blocks of 256 (24 warps) per SM
-        if (lb == 1) substep_kernel<KIND, NDIM, 128, 5><<<nb, 128, 0, s>>>(a, na, ch);        // <= 96 regs, 20 warps
-        else if (lb == 2) substep_kernel<KIND, NDIM, 128, 4><<<nb, 128, 0, s>>>(a, na, ch);   // <= 128 regs, 16 warps
-        else if (lb == 3) substep_kernel<KIND, NDIM, 256, 2><<<nb, 256, 0, s>>>(a, na, ch);   // <= 128 regs, 16 warps
-        else substep_kernel<KIND, NDIM, 256, 3><<<nb, 256, 0, s>>>(a, na, ch);
+        if (!mh) substep_kernel<KIND, NDIM, 256, 3, false><<<nb, 256, 0, s>>>(a, na, ch);
+        else if (lb == 1) substep_kernel<KIND, NDIM, 128, 5, true><<<nb, 128, 0, s>>>(a, na, ch);   // <= 96 regs
+        else if (lb == 3) substep_kernel<KIND, NDIM, 256, 2, true><<<nb, 256, 0, s>>>(a, na, ch);   // <= 128 regs
+        else substep_kernel<KIND, NDIM, 256, 3, true><<<nb, 256, 0, s>>>(a, na, ch);
     } else {
-        substep_kernel<KIND, NDIM, 256, 2><<<nb, 256, 0, s>>>(a, na, ch);
+        // hop / pair models need q >= 2 (R7), so the merged boards always apply
+        substep_kernel<KIND, NDIM, 256, 2, true><<<nb, 256, 0, s>>>(a, na, ch);
     }
     return cudaGetLastError();
 }

@@ -16,7 +16,7 @@
 
 namespace kmc {
 
-template <int TY, int TX>
+template <int TY, int TX, bool MH>
 __global__ void __launch_bounds__(256, 3)
 tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
     constexpr int SW = TX + 2;                       // smem row stride (words)
@@ -74,7 +74,7 @@ tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
         cell_of(t, lr, lc);
         const int c0 = (lr + 1) * SW + (lc + 1);
         P[0] = T[c0];
-        halo_from_words(g, T[c0 - 1], T[c0 + 1], T[c0 - SW], T[c0 + SW], hb[0], true);
+        halo_from_words<MH>(g, T[c0 - 1], T[c0 + 1], T[c0 - SW], T[c0 + SW], hb[0], true);
         gid32 = (uint32_t)((unsigned long long)(g.rep_offset + r) * (unsigned long long)g.M_global +
                            (unsigned long long)(gy0 + lr) * g.Mx + (x0 + lc));
         k = 0;
@@ -83,7 +83,7 @@ tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
     if (have) load();
     if (!__any_sync(FULL, have)) return;                          // warp beyond the tile's cells
     for (;;) {
-        const bool fin = event_step<0, 2>(a, P, hb, k, tclock, gid32, have, s_logc, s_logl);
+        const bool fin = event_step<0, 2, MH>(a, P, hb, k, tclock, gid32, have, s_logc, s_logl);
         const unsigned fm = __ballot_sync(FULL, fin);
         if (fm) {                                                   // warp-uniform
             uint32_t base = 0;
@@ -118,7 +118,8 @@ cudaError_t launch_substep_tile(const SubstepArgs& a, cudaStream_t s) {
     const int tiles_y = (g.My_local + TY - 1) / TY;
     const long long nb = (long long)tiles_x * tiles_y * g.R;
     if (nb <= 0 || nb > 0x7fffffffLL) return cudaErrorNotSupported;
-    tile_kernel_adsdes2d<TY, TX><<<(unsigned)nb, 256, 0, s>>>(a, tiles_x);
+    if (g.qx >= 2 && g.qy >= 2) tile_kernel_adsdes2d<TY, TX, true><<<(unsigned)nb, 256, 0, s>>>(a, tiles_x);
+    else tile_kernel_adsdes2d<TY, TX, false><<<(unsigned)nb, 256, 0, s>>>(a, tiles_x);
     return cudaGetLastError();
 }
 
