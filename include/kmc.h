@@ -139,6 +139,15 @@ kmc_status kmc_substep(kmc_ctx* ctx, int32_t colour, double duration);
  * sums the counters over ranks (NCCL all-reduce). */
 kmc_status kmc_observables(kmc_ctx* ctx, kmc_obs* out, uint32_t* per_cell_events);
 
+/* Two-point correlation counts (the paper's 2-point correlation function
+ * E[sigma_t(x) sigma_t(x+y)]): out_x[r] (r = 0..rmax) = number of sites x with
+ * sigma(x) = state and sigma(x + r e_x) = state, summed over the whole lattice (periodic, all
+ * replicas and ranks); out_y[r] the same along y (2D; zeros in 1D).  Divide by the number of sites
+ * for E[1{sigma(x)=s} 1{sigma(x+r)=s}].  rmax must be < the lattice width (and height in 2D); with
+ * world > 1, the y direction is limited to rmax <= q_y (one ghost cell row), else KMC_EINVAL.
+ * Synchronous; the counts are exact integers. */
+kmc_status kmc_correlation(kmc_ctx* ctx, int32_t rmax, int32_t state, int64_t* out_x, int64_t* out_y);
+
 /* Checkpoint / resume: the whole state is (lattice, window counter, time, seed, config). */
 kmc_status kmc_get_state(const kmc_ctx* ctx, uint64_t* windows, double* time);
 kmc_status kmc_set_state(kmc_ctx* ctx, uint64_t windows, double time);

@@ -61,6 +61,34 @@ def tm_coverage_1d(N, beta, K, h_dyn, ca=1.0, cd=1.0):
     return float(TN[1, 1] / np.trace(TN))
 
 
+def tm_correlation_1d(N, beta, K, h_dyn, r, ca=1.0, cd=1.0):
+    """Exact equilibrium E[sigma_0 sigma_r] of the literal rates on a periodic ring of N sites
+    (N = None: thermodynamic limit), by the transfer matrix: Tr(D T^r D T^{N-r}) / Tr(T^N)."""
+    mu = beta * h_dyn + math.log(ca / cd)
+    T = np.array([[math.exp(beta * K * a * b + mu * (a + b) / 2.0) for b in (0, 1)] for a in (0, 1)])
+    D = np.diag([0.0, 1.0])
+    if N is None:
+        w, v = np.linalg.eigh(T)
+        order = np.argsort(w)[::-1]
+        w, v = w[order], v[:, order]
+        # sum_k (w_k/w_0)^r <v0|D|vk><vk|D|v0>
+        return float(sum((w[k] / w[0]) ** r * (v[:, 0] @ D @ v[:, k]) ** 2 for k in range(2)))
+    TN = np.linalg.matrix_power(T, N)
+    return float(np.trace(D @ np.linalg.matrix_power(T, r) @ D @ np.linalg.matrix_power(T, N - r)) / np.trace(TN))
+
+
+def paper_corr1d_corrected(beta, K, h_paper, r):
+    """eq.(exactcorr1d) (P:1026-1029) read as R15: E[s_0 s_r] = c^2 + 1/4 (1 + e^{4K'} sinh^2 h')^{-1}
+    (lambda_-/lambda_+)^r, with the printed bracket for lambda_-/lambda_+ and c from eq.(exactcov1d)
+    (the printed prefactor is inverted and c^2 is missing)."""
+    Kp = beta * K / 4.0
+    hp = beta * (h_paper - K) / 2.0
+    c = paper_cov1d(beta, K, h_paper)
+    root = math.sqrt(1.0 + math.exp(4 * Kp) * math.sinh(hp) ** 2)
+    ratio = (math.exp(Kp) * math.cosh(hp) - math.exp(-Kp) * root) / (math.exp(Kp) * math.cosh(hp) + math.exp(-Kp) * root)
+    return c * c + 0.25 / (1.0 + math.exp(4 * Kp) * math.sinh(hp) ** 2) * ratio ** r
+
+
 def stationary_event_rate(ca, theta):
     """P7: in any stationary spin-flip state adsorption flux = desorption flux, so the
     event rate per site is 2 ca (1 - theta)."""

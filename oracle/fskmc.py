@@ -200,6 +200,17 @@ class FSKMC:
             return (cx[None, :] + cy[:, None]) & 1
         return (cx[None, :] & 1) + 2 * (cy[:, None] & 1)
 
+    def correlation(self, rmax: int, state: int = 1):
+        """f1: pair counts of the 2-point correlation: x[r] = #{sites x : sigma(x) =
+        sigma(x + r e_x) = state}, y[r] along y (zeros in 1D), summed over replicas; periodic."""
+        occ = self.lat == state
+        x = np.array([int((occ & np.roll(occ, -r, axis=2)).sum()) for r in range(rmax + 1)], dtype=np.int64)
+        if self.ndim == 2:
+            y = np.array([int((occ & np.roll(occ, -r, axis=1)).sum()) for r in range(rmax + 1)], dtype=np.int64)
+        else:
+            y = np.zeros(rmax + 1, dtype=np.int64)
+        return {"x": x, "y": y}
+
     def observables(self):
         lat = self.lat
         S = self.nstates

@@ -27,7 +27,7 @@ EXPORTS = [
     "kmc_run", "kmc_substep", "kmc_observables", "kmc_get_state", "kmc_set_state",
     "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
     "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
-    "kmc_set_kernel",
+    "kmc_set_kernel", "kmc_correlation",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -99,6 +99,7 @@ def lib():
         "kmc_vgroup_run": ([vp, i32, dbl, dbl, i32], i32),
         "kmc_vgroup_sync": ([vp, i32], i32),
         "kmc_set_kernel": ([vp, i32], i32),
+        "kmc_correlation": ([vp, i32, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -244,6 +245,14 @@ class KMC:
         if per_cell:
             d["per_cell_events"] = cells
         return d
+
+    def correlation(self, rmax, state=1):
+        """Two-point correlation counts (kmc_correlation): {'x': int64[rmax+1], 'y': int64[rmax+1]},
+        pairs (x, x + r e) with both sites in `state`, summed over the lattice."""
+        ox = np.zeros(int(rmax) + 1, dtype=np.int64)
+        oy = np.zeros(int(rmax) + 1, dtype=np.int64)
+        self._check(self._L.kmc_correlation(self._ctx, int(rmax), int(state), ox.ctypes.data, oy.ctypes.data))
+        return {"x": ox, "y": oy}
 
     def get_state(self):
         w, t = ctypes.c_uint64(), ctypes.c_double()

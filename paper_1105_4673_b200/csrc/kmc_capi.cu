@@ -841,6 +841,45 @@ kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
     return KMC_OK;
 }
 
+kmc_status kmc_correlation(kmc_ctx* c, int32_t rmax, int32_t state, int64_t* out_x, int64_t* out_y) {
+    if (!c || !out_x || !out_y) return fail(c, KMC_EINVAL, "NULL argument");
+    if (state < 0 || state >= c->nstates) return fail(c, KMC_EINVAL, "state %d out of range", state);
+    const long long W = c->W, H = (long long)c->g.My_local * c->g.qy * (c->world > 1 ? c->world : 1);
+    if (rmax < 0 || rmax > kMaxCorrR || rmax >= W || (c->g.ndim == 2 && rmax >= H))
+        return fail(c, KMC_EINVAL, "rmax %d out of range (< lattice extent, <= %d)", rmax, kMaxCorrR);
+    const bool do_y = c->g.ndim == 2;
+    if (do_y && c->g.ghost && rmax > c->g.qy)
+        return fail(c, KMC_EINVAL, "multi-rank y correlation needs rmax <= q_y (one ghost cell row)");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st = exchange_forward(c);
+    if (st != KMC_OK) return st;
+    const int R1 = rmax + 1;
+    unsigned long long* d = nullptr;
+    CUDA_TRY(c, cudaMallocAsync((void**)&d, (size_t)2 * R1 * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(d, 0, (size_t)2 * R1 * 8, c->stream));
+    CorrArgs a{};
+    a.g = c->g;
+    a.plane0 = c->planes[0];
+    a.plane1 = c->planes[1];
+    a.nplanes = c->nplanes;
+    a.state = state;
+    a.rmax = rmax;
+    a.do_y = do_y ? 1 : 0;
+    a.out = d;
+    CUDA_TRY(c, launch_correlation(a, c->stream));
+    if (c->world > 1 && c->comm)
+        NCCL_TRY(c, g_nccl.AllReduce(d, d, (size_t)2 * R1, ncclUint64, ncclSum, c->comm, c->stream));
+    std::vector<unsigned long long> h((size_t)2 * R1);
+    CUDA_TRY(c, cudaMemcpyAsync(h.data(), d, (size_t)2 * R1 * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaFreeAsync(d, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int r = 0; r < R1; ++r) {
+        out_x[r] = (int64_t)h[r];
+        out_y[r] = (int64_t)h[R1 + r];
+    }
+    return KMC_OK;
+}
+
 kmc_status kmc_get_state(const kmc_ctx* c, uint64_t* windows, double* time) {
     if (!c) return KMC_EINVAL;
     if (windows) *windows = c->window;

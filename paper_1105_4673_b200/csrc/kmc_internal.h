@@ -61,6 +61,16 @@ struct ObsArgs {
 
 constexpr int kObsCounters = 4 + 16 + 16;
 
+struct CorrArgs {
+    Geo g;
+    const uint64_t* plane0;
+    const uint64_t* plane1;
+    int nplanes, state, rmax, do_y;
+    unsigned long long* out;         // [2][rmax+1]: pair counts along x, then y
+};
+constexpr int kMaxCorrR = 1024;      // largest rmax of kmc_correlation
+cudaError_t launch_correlation(const CorrArgs& a, cudaStream_t s);
+
 // kernels.cu
 cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cudaStream_t s);
 cudaError_t launch_substep_tile(const SubstepArgs& a, cudaStream_t s);   // kmc_tile.cu (2D spin flip)

@@ -286,6 +286,105 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
         if (sh[i]) atomicAdd(&a.out[i], sh[i]);
 }
 
+// ---------------------------------------------------------------------------------------------
+// f1: two-point correlation counts.  For a displacement r = a q + b along x (y), the partner of
+// every site of a cell lies in the cells a and a+1 further along the axis; the partner board is
+// assembled from those two words with shifts and column (row) masks and AND-ed with the cell's
+// own state board.  Warp-reduced per r (redux.sync), then one shared and one global atomic.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t state_board(const CorrArgs& a, long long idx) {
+    const uint64_t p0 = a.plane0[idx];
+    if (a.nplanes == 1) return a.state == 1 ? p0 : (a.g.valid & ~p0);
+    const uint64_t p1 = a.plane1[idx];
+    return a.state == 1 ? p0 : a.state == 2 ? p1 : (a.g.valid & ~(p0 | p1));
+}
+
+__global__ void __launch_bounds__(256) correlation_kernel(const CorrArgs a) {
+    extern __shared__ unsigned long long sc[];            // [2][rmax+1]
+    const Geo& g = a.g;
+    const int R1 = a.rmax + 1;
+    for (int i = threadIdx.x; i < 2 * R1; i += blockDim.x) sc[i] = 0;
+    __syncthreads();
+    const long long rowlen = (long long)g.R * g.Mx;
+    const long long ncell = (long long)g.My_local * rowlen;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // warp-uniform trip count: every lane of a warp runs the same iterations (redux needs all 32)
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < ncell; base += stride) {
+        const long long t = base + threadIdx.x;
+        const bool ok = t < ncell;
+        int cx = 0, r = 0, cy = 0;
+        if (ok) {
+            cx = (int)(t % g.Mx);
+            const long long rest = t / g.Mx;
+            r = (int)(rest % g.R);
+            cy = (int)(rest / g.R);
+        }
+        const int sy = cy + g.ghost;
+        const long long rb = (long long)r * g.Mx;
+        const uint64_t A = ok ? state_board(a, (long long)sy * rowlen + rb + cx) : 0ull;
+        // ---- along x ----
+        {
+            int aa = 0;
+            uint64_t W0 = A, W1 = ok ? state_board(a, (long long)sy * rowlen + rb + (cx + 1) % g.Mx) : 0ull;
+            for (int rr = 0, b = 0; rr < R1; ++rr) {
+                uint64_t S;
+                if (b == 0) S = W0;
+                else {
+                    const uint64_t lowcols = ((1ull << (g.qx - b)) - 1ull) * g.col0;   // columns < qx-b
+                    S = ((W0 >> b) & lowcols) | ((W1 << (g.qx - b)) & (g.valid & ~lowcols));
+                }
+                const uint32_t v = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(A & S));
+                if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sc[rr], (unsigned long long)v);
+                if (++b == g.qx) {                           // next whole cell
+                    b = 0;
+                    ++aa;
+                    W0 = W1;
+                    W1 = ok ? state_board(a, (long long)sy * rowlen + rb + (cx + aa + 1) % g.Mx) : 0ull;
+                }
+            }
+        }
+        // ---- along y ----
+        if (a.do_y) {
+            auto rowidx = [&](int k) -> long long {           // storage row of the cell k rows below
+                int yy = sy + k;
+                if (!g.ghost) yy %= g.My_local;
+                return (long long)yy * rowlen + rb + cx;
+            };
+            int aa = 0;
+            uint64_t W0 = A, W1 = ok ? state_board(a, rowidx(1)) : 0ull;
+            for (int rr = 0, b = 0; rr < R1; ++rr) {
+                uint64_t S;
+                if (b == 0) S = W0;
+                else S = ((W0 >> (b * g.qx)) | (W1 << ((g.qy - b) * g.qx))) & g.valid;
+                const uint32_t v = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(A & S));
+                if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sc[R1 + rr], (unsigned long long)v);
+                if (++b == g.qy) {
+                    b = 0;
+                    ++aa;
+                    W0 = W1;
+                    if (rr + 2 < R1) W1 = ok ? state_board(a, rowidx(aa + 1)) : 0ull;   // needed only if b > 0 follows
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * R1; i += blockDim.x)
+        if (sc[i]) atomicAdd(&a.out[i], sc[i]);
+}
+
+cudaError_t launch_correlation(const CorrArgs& a, cudaStream_t s) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long ncell = (long long)a.g.My_local * a.g.R * a.g.Mx;
+    long long nb = (ncell + 255) / 256;
+    if (nb > 8LL * nsm) nb = 8LL * nsm;
+    if (nb < 1) nb = 1;
+    const size_t smem = (size_t)2 * (a.rmax + 1) * sizeof(unsigned long long);
+    correlation_kernel<<<(unsigned)nb, 256, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);

@@ -276,3 +276,22 @@ def test_virtual_ranks_bit_identical(kind, params, scheme, dt, cell, world):
     assert a["events"] == b["events"] > 0
     for key in ("n_state", "nn_pairs", "n_state_by_colour"):
         assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.parametrize("ndim,dims,cell,kind,R,rmax", [
+    (2, (64, 96), (8, 8), "adsdes", 2, 40),
+    (2, (48, 40), (4, 2), "zgb", 3, 39),
+    (1, (512,), (32,), "adsdes", 4, 100),
+    (1, (256,), (4,), "zgb", 2, 70),
+])
+def test_correlation_counts_match_oracle(ndim, dims, cell, kind, R, rmax):
+    """f1: kmc_correlation pair counts equal the oracle's numpy definition (every state, x and y)."""
+    gpu, orc = make_pair(ndim, dims, cell, kind, {}, 0, R)
+    lat = (si.bernoulli_lattice(gpu.local_shape, 0.45, seed=8) if kind == "adsdes"
+           else si.categorical_lattice(gpu.local_shape, [0.4, 0.35, 0.25], seed=8))
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    for state in range(gpu.nstates):
+        a, b = gpu.correlation(rmax, state), orc.correlation(rmax, state)
+        assert np.array_equal(a["x"], b["x"]), (state, "x")
+        assert np.array_equal(a["y"], b["y"]), (state, "y")

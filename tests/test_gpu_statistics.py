@@ -200,3 +200,23 @@ def test_conservation_and_zgb_coverage_sum():
     z.run(5.0, 0.1, "lie")
     o = z.observables()
     assert o["events"] > 0 and abs(o["coverage"][:3].sum() - 1.0) < 1e-12
+
+
+def test_1d_two_point_correlation_vs_exact():
+    """Fig.`phasediag1D`(b): equilibrium E[s_0 s_r] at h = 1, beta = 2, 4 on
+    N = 65536 at dt = 1 equals the exact 1D correlation (R15 reading of eq.(exactcorr1d) = TM)."""
+    kmc = _kmc()
+    K, hp = 1.0, 1.0
+    for beta in (2.0, 4.0):
+        hd = exact.h_dyn_from_paper(hp, K, 1)
+        g = kmc.KMC(1, (65536,), (32,), kind="adsdes", replicas=4, seed=21, ca=1.0, cd=1.0, beta=beta, K=K, h=hd)
+        g.set_config(si.bernoulli_lattice(g.local_shape, 0.5, seed=3))
+        g.run(100.0, 1.0, "lie")
+        samples = []
+        for _ in range(60):
+            g.run(2.0, 1.0, "lie")
+            samples.append(g.correlation(10)["x"] / (4 * 65536))
+        s = np.array(samples).reshape(6, 10, 11).mean(axis=1)           # batch means
+        m, se = s.mean(axis=0), s.std(axis=0, ddof=1) / math.sqrt(6)
+        ex = np.array([exact.paper_corr1d_corrected(beta, K, hp, r) for r in range(11)])
+        assert np.all(np.abs(m - ex) <= np.maximum(4 * se, 3e-3)), (beta, m - ex, se)

@@ -152,3 +152,40 @@ def test_lie_order_asymmetric_start():
     es = [abs(bf.law(p0, Q, Qc, "strang", dt, 2.0, 2) @ cov - ex) for dt in (0.25, 0.125)]
     assert 1.6 < el[0] / el[1] < 2.5
     assert 3.2 < es[0] / es[1] < 5.0
+
+
+def test_tm_correlation_vs_bruteforce_and_paper_R15():
+    """f1 pins: the finite-N transfer-matrix E[s_0 s_r] equals the brute-force stationary law of the
+    literal rates (N = 8 ring), and the R15 reading of eq.(exactcorr1d) equals the N -> infinity TM."""
+    N = 8
+    lat = bf.Lattice(1, 1, N, 1, 2, 2)
+    m = ising(beta=1.7, K=1.0, h=-0.6, ca=1.0, cd=0.9)
+    Q, Qc, S = bf.generators(m, lat)
+    w, v = np.linalg.eig(Q.toarray().T)
+    pi = np.real(v[:, np.argmin(np.abs(w))])
+    pi /= pi.sum()
+    import itertools
+    confs = np.array(list(itertools.product(range(2), repeat=N)))[:, ::-1]
+    for r in range(0, 5):
+        bfv = pi @ (confs[:, 0] * confs[:, r % N])
+        assert abs(bfv - exact.tm_correlation_1d(N, 1.7, 1.0, -0.6, r, 1.0, 0.9)) < 1e-12
+    for beta, hp in ((2.0, 1.0), (4.0, 1.0), (1.0, 0.3)):
+        hd = exact.h_dyn_from_paper(hp, 1.0, 1)
+        for r in (0, 1, 2, 5, 9):
+            assert abs(exact.paper_corr1d_corrected(beta, 1.0, hp, r) - exact.tm_correlation_1d(None, beta, 1.0, hd, r)) < 1e-12
+
+
+def test_oracle_correlation_counts_by_definition():
+    """FSKMC.correlation counts equal a direct double loop over sites (definition)."""
+    from oracle.fskmc import FSKMC, model_params
+    rng = np.random.default_rng(5)
+    o = FSKMC(2, (8, 12), (2, 2), "zgb", model_params(), replicas=2)
+    o.set_config(rng.integers(0, 3, (2, 8, 12)).astype(np.uint8))
+    for state in (0, 1, 2):
+        c = o.correlation(7, state)
+        for r in range(8):
+            bx = sum(int(o.lat[k, y, x] == state and o.lat[k, y, (x + r) % 12] == state)
+                     for k in range(2) for y in range(8) for x in range(12))
+            by = sum(int(o.lat[k, y, x] == state and o.lat[k, (y + r) % 8, x] == state)
+                     for k in range(2) for y in range(8) for x in range(12))
+            assert c["x"][r] == bx and c["y"][r] == by
