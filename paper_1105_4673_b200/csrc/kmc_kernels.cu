@@ -224,7 +224,11 @@ cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cu
 // a8: observables.  Counters (u64): [0..3] n_state, [4..19] by colour [c*4+s],
 // [20..35] ordered nearest-neighbour bonds (x, x+e) for e in {+x, +y}: [20 + a*4 + b].
 // ---------------------------------------------------------------------------------------------
+template <int NP, int NDIM>
 __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
+    // NP planes and NDIM fixed at compile time, so every counter index is static and the 36
+    // per-thread counters live in registers (no local-memory array)
+    constexpr int NS = NP + 1;
     const Geo& g = a.g;
     __shared__ unsigned long long sh[kObsCounters];
     for (int i = threadIdx.x; i < kObsCounters; i += blockDim.x) sh[i] = 0;
@@ -232,47 +236,49 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
     uint32_t acc[kObsCounters];
 #pragma unroll
     for (int i = 0; i < kObsCounters; ++i) acc[i] = 0;
-    const long long rowlen = (long long)g.R * g.Mx;
-    const long long ncell = (long long)g.My_local * rowlen;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int cx = (int)(t % g.Mx);
-        const long long rest = t / g.Mx;
-        const int r = (int)(rest % g.R);
-        const int cy = (int)(rest / g.R);
-        const int sy = cy + g.ghost;
+    const uint32_t rowlen = (uint32_t)g.R * g.Mx;
+    const uint32_t ncell = (uint32_t)g.My_local * rowlen;
+    const double inv_mx = 1.0 / (double)g.Mx, inv_r = 1.0 / (double)g.R;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += gridDim.x * blockDim.x) {
+        uint32_t rest, cx, cy, r;
+        fast_divmod(t, (uint32_t)g.Mx, inv_mx, rest, cx);
+        fast_divmod(rest, (uint32_t)g.R, inv_r, cy, r);
+        const int sy = (int)cy + g.ghost;
         int syS = sy + 1;
         if (!g.ghost && syS >= g.My_local) syS -= g.My_local;
-        const int cxE = cx == g.Mx - 1 ? 0 : cx + 1;
-        const long long iC = (long long)sy * rowlen + (long long)r * g.Mx + cx;
-        const long long iE = (long long)sy * rowlen + (long long)r * g.Mx + cxE;
-        const long long iS = (long long)syS * rowlen + (long long)r * g.Mx + cx;
-        uint64_t A[3], Bx[3], By[3];
-        const uint64_t notcolL = g.valid & ~g.colL;
+        const uint32_t cxE = cx == (uint32_t)g.Mx - 1 ? 0 : cx + 1;
+        const uint32_t rb = r * g.Mx;
+        const uint32_t iC = (uint32_t)sy * rowlen + rb + cx;
+        const uint32_t iE = (uint32_t)sy * rowlen + rb + cxE;
+        const uint32_t iS = (uint32_t)syS * rowlen + rb + cx;
+        uint64_t A[NS], Bx[NS], By[NS];
         uint64_t occ = 0, occx = 0, occy = 0;
-        for (int p = 0; p < a.nplanes; ++p) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
             const uint64_t* pl = p == 0 ? a.plane0 : a.plane1;
             const uint64_t P = pl[iC];
             A[1 + p] = P;
-            Bx[1 + p] = ((P >> 1) & notcolL) | ((pl[iE] << (g.qx - 1)) & g.colL);
-            By[1 + p] = (g.ndim == 2) ? ((P >> g.qx) | ((pl[iS] << g.shN) & g.rowL)) : 0;
+            Bx[1 + p] = ((P >> 1) & g.notcolL) | ((pl[iE] << (g.qx - 1)) & g.colL);   // sigma(x+1)
+            By[1 + p] = NDIM == 2 ? ((P >> g.qx) | ((pl[iS] << g.shN) & g.rowL)) : 0;  // sigma(y+1)
             occ |= A[1 + p]; occx |= Bx[1 + p]; occy |= By[1 + p];
         }
         A[0] = g.valid & ~occ;
         Bx[0] = g.valid & ~occx;
         By[0] = g.valid & ~occy;
-        const int ns = a.nplanes + 1;
-        const int gy = g.row_offset + cy;
+        const uint32_t gy = g.row_offset + cy;
         int colour;
-        if (a.C == 2) colour = g.ndim == 1 ? (cx & 1) : ((cx + gy) & 1);
-        else colour = (cx & 1) + 2 * (gy & 1);
-        for (int s = 0; s < ns; ++s) {
+        if (a.C == 2) colour = NDIM == 1 ? (int)(cx & 1) : (int)((cx + gy) & 1);
+        else colour = (int)(cx & 1) + 2 * (int)(gy & 1);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
             const uint32_t c = __popcll(A[s]);
             acc[s] += c;
-            acc[4 + colour * 4 + s] += c;
-            for (int b = 0; b < ns; ++b) {
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) acc[4 + cc * 4 + s] += colour == cc ? c : 0u;
+#pragma unroll
+            for (int b = 0; b < NS; ++b) {
                 acc[20 + s * 4 + b] += __popcll(A[s] & Bx[b]);
-                if (g.ndim == 2) acc[20 + s * 4 + b] += __popcll(A[s] & By[b]);
+                if (NDIM == 2) acc[20 + s * 4 + b] += __popcll(A[s] & By[b]);
             }
         }
     }
@@ -393,7 +399,13 @@ cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s) {
     long long nb = (ncell + 255) / 256;
     if (nb > 4LL * nsm) nb = 4LL * nsm;
     if (nb < 1) nb = 1;
-    observables_kernel<<<(unsigned)nb, 256, 0, s>>>(a);
+    if (a.nplanes == 1) {
+        if (a.g.ndim == 2) observables_kernel<1, 2><<<(unsigned)nb, 256, 0, s>>>(a);
+        else observables_kernel<1, 1><<<(unsigned)nb, 256, 0, s>>>(a);
+    } else {
+        if (a.g.ndim == 2) observables_kernel<2, 2><<<(unsigned)nb, 256, 0, s>>>(a);
+        else observables_kernel<2, 1><<<(unsigned)nb, 256, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
