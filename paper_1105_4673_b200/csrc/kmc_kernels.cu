@@ -203,8 +203,12 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
         else if (lb == 3) substep_kernel<KIND, NDIM, 256, 2, true><<<nb, 256, 0, s>>>(a, na, ch);   // <= 128 regs
         else substep_kernel<KIND, NDIM, 256, 3, true><<<nb, 256, 0, s>>>(a, na, ch);
     } else {
-        // hop / pair models need q >= 2 (R7), so the merged boards always apply
-        substep_kernel<KIND, NDIM, 256, 2, true><<<nb, 256, 0, s>>>(a, na, ch);
+        // hop / pair models need q >= 2 (R7), so the merged boards always apply.  Measured on B200:
+        // diffusion (22 masks live) is fastest with <= 128 registers (2 CTAs/SM), ZGB (counts +
+        // rebuilt mask) with <= 80 registers (3 CTAs/SM).  KMC_LB=3 forces 128, KMC_LB=4 forces 80.
+        const bool big = (KIND == 1 && lb != 4) || lb == 3;
+        if (big) substep_kernel<KIND, NDIM, 256, 2, true><<<nb, 256, 0, s>>>(a, na, ch);
+        else substep_kernel<KIND, NDIM, 256, 3, true><<<nb, 256, 0, s>>>(a, na, ch);
     }
     return cudaGetLastError();
 }
