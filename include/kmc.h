@@ -129,6 +129,16 @@ kmc_status kmc_get_config_device(kmc_ctx* ctx, uint8_t* dev_local_slab, int64_t 
  * colour xi_w drawn from Philox by global window id (R4).  Asynchronous. */
 kmc_status kmc_run(kmc_ctx* ctx, double T, double dt, kmc_scheme scheme);
 
+/* Temporal multiscale Strang (eq.(strang3)): per macro-step d,
+ *   e^{d/2 L_slow} [ e^{(d/n_fast) L_fast} ]^{n_fast} e^{d/2 L_slow},
+ * every factor itself split over the colours with the `inner` scheme (Lie, Strang or random, as in
+ * kmc_run) -- the spatio-temporal hierarchy of P:750-753.  fast_classes: bit i = class i of the rate
+ * table is fast (0 = the hop classes, e.g. ZGB_DIFF's CO diffusion).  Windows of one
+ * mechanism run with the other mechanism's rates set to 0.  KMC_EINVAL when the fast set is empty or
+ * covers every class; KMC_WTRUNCATED as kmc_run.  Asynchronous. */
+kmc_status kmc_run_multiscale(kmc_ctx* ctx, double T, double dt, int32_t n_fast, kmc_scheme inner,
+                              uint64_t fast_classes);
+
 /* One window: every cell of colour `colour` runs its SSA for `duration` (eq.(exact)); the window
  * counter advances by one, physical time does not.  Asynchronous. */
 kmc_status kmc_substep(kmc_ctx* ctx, int32_t colour, double duration);

@@ -82,8 +82,14 @@ def _events(model, lat, conf, i):
     return ev
 
 
-def generators(model, lat):
-    """Return (Q, [Q^0..Q^{C-1}], S) as sparse CSR matrices; Q = sum_c Q^c."""
+def _is_hop(i, upd):
+    """Diffusion events move a particle: the anchor empties and one neighbour fills (state 1)."""
+    return len(upd) == 2 and upd[i] == 0 and any(j != i and v == 1 for j, v in upd.items())
+
+
+def generators(model, lat, mech=None):
+    """Return (Q, [Q^0..Q^{C-1}], S) as sparse CSR matrices; Q = sum_c Q^c.
+    mech = "fast" keeps only diffusion (hop) events, "slow" only the others (eq.(fastslow))."""
     S = 2 if model["kind"] in ("adsdes", "adsdes_diff") else 3
     N = lat.N
     nconf = S ** N
@@ -97,6 +103,8 @@ def generators(model, lat):
             c = lat.colour(i)
             for rate, upd in _events(model, lat, conf, i):
                 if rate == 0.0:
+                    continue
+                if mech is not None and (mech == "fast") != _is_hop(i, upd):
                     continue
                 to = idx + sum((v - conf[j]) * powers[j] for j, v in upd.items())
                 rows[c].append(idx); cols[c].append(to); vals[c].append(rate)
@@ -141,6 +149,27 @@ def law(p0, Q, Qc, scheme, dt, T, C):
                 p = sum(evolve(p, Qc[c], dt) for c in range(C)) / C
         else:
             raise ValueError(scheme)
+    return p
+
+
+def _inner(inner, C, d):
+    if inner == "lie":
+        return [(c, d) for c in range(C)]
+    h = d / 2
+    if C == 2:
+        return [(0, h), (1, d), (0, h)]
+    return [(0, h), (1, h), (2, h), (3, d), (2, h), (1, h), (0, h)]
+
+
+def law_multiscale(p0, Qslow_c, Qfast_c, dt, T, n_fast, inner, C):
+    """Exact law of the spatio-temporal scheme of eq.(strang3): per macro-step
+    e^{dt/2 L_slow} [e^{(dt/n) L_fast}]^n e^{dt/2 L_slow}, each factor split over the colours by the
+    deterministic `inner` scheme ('lie' or 'strang')."""
+    p = p0.copy()
+    for _ in range(int(round(T / dt))):
+        for dur, Qs in [(dt / 2, Qslow_c)] + [(dt / n_fast, Qfast_c)] * n_fast + [(dt / 2, Qslow_c)]:
+            for c, d in _inner(inner, C, dur):
+                p = evolve(p, Qs[c], d)
     return p
 
 

@@ -146,14 +146,21 @@ class FSKMC:
         return self.lat.copy()
 
     # -- one window: eq.(exact) --------------------------------------------
-    def substep(self, colour: int, D: float) -> int:
+    def substep(self, colour: int, D: float, classes=None) -> int:
+        """One window; `classes` (optional set of class indices) restricts the window to those
+        mechanisms -- the other classes' rates are 0 (multiscale sub-steps, eq.(strang3))."""
         t = self.table
         ip = ctypes.POINTER(ctypes.c_int)
+        rates = t["rate_u64"].copy()
+        if classes is not None:
+            for i in range(t["n"]):
+                if i not in classes:
+                    rates[i] = 0
         ev = lib().orc_window(
             self.lat.ctypes.data, self.R, self.H, self.W, self.ndim, self.qx, self.qy,
             self.C, int(colour), float(D), self.window, self.seed,
             t["n"], t["type"].ctypes.data_as(ip), t["dir"].ctypes.data_as(ip),
-            t["kappa"].ctypes.data_as(ip), t["rate_u64"].ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+            t["kappa"].ctypes.data_as(ip), rates.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
             t["F"], self.W_events.ctypes.data)
         self.window += 1
         self.events += int(ev)
@@ -188,6 +195,28 @@ class FSKMC:
         durs, truncated = macro_steps(T, dt)
         for d in durs:
             self.macro_step(sc, d)
+        return truncated
+
+    def run_multiscale(self, T: float, dt: float, n_fast: int, inner="lie", fast_classes=None) -> bool:
+        """f2, eq.(strang3): per macro-step d, e^{d/2 L_slow} [e^{(d/n) L_fast}]^n
+        e^{d/2 L_slow}, each factor split over the colours with the `inner` scheme.
+        Fast classes default to the hop slot types (R12 diffusion / ZGB CO diffusion)."""
+        sc = SCHEME[inner] if isinstance(inner, str) else int(inner)
+        n = self.table["n"]
+        if fast_classes is None:
+            fast = {i for i in range(n) if int(self.table["type"][i]) in (2, 7)}   # T_HOP, T_COHOP
+        else:
+            fast = set(fast_classes)
+        slow = set(range(n)) - fast
+        if not fast or not slow:
+            raise ValueError("multiscale needs a non-empty proper subset of fast classes")
+        durs, truncated = macro_steps(T, dt)
+        for d in durs:
+            h, df = d * 0.5, d / n_fast
+            for dur, cls in [(h, slow)] + [(df, fast)] * n_fast + [(h, slow)]:
+                for colour, D in substeps(sc, self.C, dur, self.seed, self.window):
+                    self.substep(colour, D, cls)
+            self.time += d
         return truncated
 
     # -- a8 observables ----------------------------------------------------

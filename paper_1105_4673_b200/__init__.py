@@ -27,7 +27,7 @@ EXPORTS = [
     "kmc_run", "kmc_substep", "kmc_observables", "kmc_get_state", "kmc_set_state",
     "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
     "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
-    "kmc_set_kernel", "kmc_correlation",
+    "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -100,6 +100,7 @@ def lib():
         "kmc_vgroup_sync": ([vp, i32], i32),
         "kmc_set_kernel": ([vp, i32], i32),
         "kmc_correlation": ([vp, i32, i32, vp, vp], i32),
+        "kmc_run_multiscale": ([vp, dbl, dbl, i32, i32, u64], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -219,6 +220,14 @@ class KMC:
         """kmc_run; returns True if the last macro-step was shortened (KMC_WTRUNCATED)."""
         sc = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
         st = self._check(self._L.kmc_run(self._ctx, float(T), float(dt), sc), allow=(KMC_WTRUNCATED,))
+        return st == KMC_WTRUNCATED
+
+    def run_multiscale(self, T, dt, n_fast, inner="lie", fast_classes=0):
+        """kmc_run_multiscale (eq.(strang3)): e^{dt/2 L_slow} [e^{dt/n L_fast}]^n e^{dt/2 L_slow}
+        per macro-step, each factor split over colours with `inner`; returns the truncation flag."""
+        sc = SCHEMES[inner] if isinstance(inner, str) else int(inner)
+        st = self._check(self._L.kmc_run_multiscale(self._ctx, float(T), float(dt), int(n_fast), sc,
+                                                    int(fast_classes)), allow=(KMC_WTRUNCATED,))
         return st == KMC_WTRUNCATED
 
     def substep(self, colour, duration):

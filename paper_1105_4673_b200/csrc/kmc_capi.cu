@@ -280,7 +280,9 @@ kmc_status exchange_reverse(kmc_ctx* c) {
 }
 
 // One window's kernel (a3-a6) on this rank's owned cells of `colour`; advances the window counter.
-kmc_status launch_window(kmc_ctx* c, int colour, double D) {
+// class_mask: bit i set = class i active in this window (multiscale sub-steps, f2); the rates of
+// inactive classes are 0, so they never fire and add nothing to lambda.
+kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull) {
     SubstepArgs a{};
     a.g = c->g;
     a.plane0 = c->planes[0];
@@ -301,7 +303,7 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D) {
     }
     a.w_lo = (uint32_t)c->window;
     a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
-    for (int i = 0; i < c->nclass; ++i) a.rate[i] = c->crate_u64[i];
+    for (int i = 0; i < c->nclass; ++i) a.rate[i] = ((class_mask >> i) & 1ull) ? c->crate_u64[i] : 0ull;
     for (int j = 0; j < kLogTab; ++j) {   // log_spec tables, host libm
         a.log_c[j] = 128.0 / (double)(j + 91);
         a.log_l[j] = -std::log(a.log_c[j]);
@@ -342,12 +344,12 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D) {
     return KMC_OK;
 }
 
-kmc_status do_substep(kmc_ctx* c, int colour, double D) {
+kmc_status do_substep(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull) {
     if (colour < 0 || colour >= c->C) return fail(c, KMC_EINVAL, "colour %d out of range [0,%d)", colour, c->C);
     if (!(D >= 0.0)) return fail(c, KMC_EINVAL, "window duration must be >= 0");
     kmc_status st = exchange_forward(c);
     if (st != KMC_OK) return st;
-    st = launch_window(c, colour, D);
+    st = launch_window(c, colour, D, class_mask);
     if (st != KMC_OK) return st;
     return exchange_reverse(c);
 }
@@ -725,6 +727,42 @@ kmc_status kmc_run(kmc_ctx* c, double T, double dt, kmc_scheme scheme) {
             kmc_status st = do_substep(c, sd.first, sd.second);
             if (st != KMC_OK) return st;
         }
+        c->time += d;
+    }
+    return truncated ? KMC_WTRUNCATED : KMC_OK;
+}
+
+kmc_status kmc_run_multiscale(kmc_ctx* c, double T, double dt, int32_t n_fast, kmc_scheme inner,
+                              uint64_t fast_classes) {
+    if (!c) return KMC_EINVAL;
+    if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: multiscale runs are not grouped");
+    if (!(dt > 0.0) || !(T >= 0.0) || std::isinf(T)) return fail(c, KMC_EINVAL, "need dt > 0 and finite T >= 0");
+    if (n_fast < 1) return fail(c, KMC_EINVAL, "n_fast must be >= 1");
+    if (inner < KMC_LIE || inner > KMC_RANDOM) return fail(c, KMC_EINVAL, "unknown inner scheme %d", (int)inner);
+    const uint64_t all = c->nclass >= 64 ? ~0ull : ((1ull << c->nclass) - 1ull);
+    if (fast_classes == 0)   // default: the hop mechanisms (R12 diffusion, ZGB CO diffusion)
+        for (int i = 0; i < c->nclass; ++i)
+            if (c->ctype[i] == T_HOP || c->ctype[i] == T_COHOP) fast_classes |= 1ull << i;
+    fast_classes &= all;
+    if (fast_classes == 0 || fast_classes == all)
+        return fail(c, KMC_EINVAL, "multiscale needs a non-empty proper subset of fast classes");
+    const uint64_t slow = all & ~fast_classes;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    bool truncated = false;
+    for (double d : macro_durations(T, dt, &truncated)) {
+        // eq.(strang3): e^{d/2 L_r} [e^{(d/N) L_f}]^N e^{d/2 L_r}, each factor split over colours
+        const double h = d * 0.5, df = d / (double)n_fast;
+        auto factor = [&](double dur, uint64_t mask) -> kmc_status {
+            for (const auto& sd : macro_schedule(inner, c->C, dur, c->geom.seed, c->window)) {
+                kmc_status st = do_substep(c, sd.first, sd.second, mask);
+                if (st != KMC_OK) return st;
+            }
+            return KMC_OK;
+        };
+        kmc_status st = factor(h, slow);
+        for (int i = 0; i < n_fast && st == KMC_OK; ++i) st = factor(df, fast_classes);
+        if (st == KMC_OK) st = factor(h, slow);
+        if (st != KMC_OK) return st;
         c->time += d;
     }
     return truncated ? KMC_WTRUNCATED : KMC_OK;

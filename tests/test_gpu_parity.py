@@ -295,3 +295,22 @@ def test_correlation_counts_match_oracle(ndim, dims, cell, kind, R, rmax):
         a, b = gpu.correlation(rmax, state), orc.correlation(rmax, state)
         assert np.array_equal(a["x"], b["x"]), (state, "x")
         assert np.array_equal(a["y"], b["y"]), (state, "y")
+
+
+@pytest.mark.parametrize("ndim,dims,cell,kind,params,inner,nf", [
+    (2, (64, 64), (4, 4), "adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=8.0), "lie", 4),
+    (2, (32, 64), (4, 8), "zgb_diff", dict(k1=0.45, k2=1.0, c_hop=10.0), "strang", 5),
+    (1, (256,), (4,), "adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-1.0, c_hop=5.0), "random", 3),
+])
+def test_multiscale_bit_exact(ndim, dims, cell, kind, params, inner, nf):
+    """f2: kmc_run_multiscale (eq.(strang3), fast hops sub-cycled) is bit-exact vs O2."""
+    gpu, orc = make_pair(ndim, dims, cell, kind, params, 0, 2)
+    lat = (si.bernoulli_lattice(gpu.local_shape, 0.4, seed=12) if kind == "adsdes_diff"
+           else si.categorical_lattice(gpu.local_shape, [0.5, 0.3, 0.2], seed=12))
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    for _ in range(2):
+        gpu.run_multiscale(1.0, 0.5, nf, inner)
+        orc.run_multiscale(1.0, 0.5, nf, inner)
+        assert_same_state(gpu, orc, f"multiscale {kind} {inner}")
+    assert orc.events > 0

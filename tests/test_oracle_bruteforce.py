@@ -189,3 +189,23 @@ def test_oracle_correlation_counts_by_definition():
             by = sum(int(o.lat[k, y, x] == state and o.lat[k, (y + r) % 8, x] == state)
                      for k in range(2) for y in range(8) for x in range(12))
             assert c["x"][r] == bx and c["y"][r] == by
+
+
+def test_multiscale_generator_split_and_order():
+    """f2 (eq.(fastslow), eq.(strang3)): L = L_fast + L_slow exactly (per colour), and the
+    spatio-temporal scheme with Strang inside is second order: halving dt quarters the global error."""
+    lat = bf.Lattice(1, 1, 6, 1, 2, 2)
+    m = dict(kind="adsdes_diff", ca=0.4, cd=0.6, beta=1.0, K=1.0, h=-1.0, c_hop=3.0)
+    Q, Qc, S = bf.generators(m, lat)
+    Qf, Qfc, _ = bf.generators(m, lat, mech="fast")
+    Qs, Qsc, _ = bf.generators(m, lat, mech="slow")
+    assert abs(Q - Qf - Qs).max() < 1e-12
+    for c in range(2):
+        assert abs(Qc[c] - Qfc[c] - Qsc[c]).max() < 1e-12
+        assert abs(Qfc[c]).max() > 0 and abs(Qsc[c]).max() > 0
+    start = [1, 1, 0, 0, 1, 0]
+    p0 = bf.point_mass(S, 6, start)
+    cov = bf.coverage_values(lat, S, sites=[0, 1])           # a sub-lattice observable (P5)
+    ex = bf.law(p0, Q, Qc, "exact", 0, 1.0, 2) @ cov
+    e = [abs(bf.law_multiscale(p0, Qsc, Qfc, dt, 1.0, 3, "strang", 2) @ cov - ex) for dt in (0.25, 0.125)]
+    assert 3.0 < e[0] / e[1] < 5.5, e

@@ -193,3 +193,20 @@ def test_o1_noninteracting_closed_form():
     for k, t in enumerate([0.5, 1.0, 4.0]):
         th = exact.noninteracting_theta(t, 1.0, 0.5)
         assert abs(snap[k].mean() - th) <= Z * math.sqrt(th * (1 - th) / 4096)
+
+
+@pytest.mark.parametrize("inner", ["lie", "strang"])
+def test_o2_multiscale_law(inner):
+    """f2: O2's spatio-temporal scheme (eq.(strang3)) samples the brute-force law exactly."""
+    N, q, dt, T, R, nf = 8, 2, 0.5, 1.0, 20000, 3
+    p = dict(ca=0.4, cd=0.6, beta=1.0, K=1.0, h=-1.0, c_hop=3.0)
+    lat = bf.Lattice(1, 1, N, 1, q, 2)
+    m = bf_model("adsdes_diff", p)
+    Qf, Qfc, S = bf.generators(m, lat, mech="fast")
+    Qs, Qsc, _ = bf.generators(m, lat, mech="slow")
+    start = np.array([1, 1, 0, 0, 1, 0, 0, 1], np.uint8)
+    law = bf.law_multiscale(bf.point_mass(S, N, start), Qsc, Qfc, dt, T, nf, inner, 2)
+    sim = FSKMC(1, (N,), (q,), "adsdes_diff", model_params(**p), colours=2, replicas=R, seed=31)
+    sim.set_config(np.broadcast_to(start, (R, 1, N)))
+    sim.run_multiscale(T, dt, nf, inner)
+    check_law(confs_index(sim.get_config(), S), law)
