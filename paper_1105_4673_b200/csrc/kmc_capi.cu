@@ -121,6 +121,7 @@ struct kmc_ctx {
     bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
     double tile_rate_bound = 0.0;            // rough events per unit time per cell (kernel choice)
     int kernel_mode = 0;                     // kmc_set_kernel
+    SubstepArgs args{};                      // window-invariant kernel arguments (build_args_template)
     struct VgShared* vg_shared = nullptr;    // virtual-rank group stream (reference counted)
     // schedule state
     uint64_t window = 0;
@@ -282,16 +283,15 @@ kmc_status exchange_reverse(kmc_ctx* c) {
 // One window's kernel (a3-a6) on this rank's owned cells of `colour`; advances the window counter.
 // class_mask: bit i set = class i active in this window (multiscale sub-steps, f2); the rates of
 // inactive classes are 0, so they never fire and add nothing to lambda.
-kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull) {
-    SubstepArgs a{};
+// The window-invariant kernel arguments (geometry, keys, Philox round keys, rate table, log
+// tables), built once at create so a window launch only fills in colour, duration and window id.
+void build_args_template(kmc_ctx* c) {
+    SubstepArgs& a = c->args;
+    a = SubstepArgs{};
     a.g = c->g;
-    a.plane0 = c->planes[0];
-    a.plane1 = c->planes[1];
     a.wev = c->wev;
     a.ev_total = c->ev_total;
-    a.colour = colour;
     a.C = c->C;
-    a.D = D;
     a.inv_scale = std::ldexp(1.0, -c->F);
     a.inv_half = 1.0 / (double)(c->g.Mx / 2);
     a.inv_R = 1.0 / (double)c->g.R;
@@ -301,9 +301,7 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
         a.rk0[i] = a.key0 + (uint32_t)i * 0x9E3779B9u;
         a.rk1[i] = a.key1 + (uint32_t)i * 0xBB67AE85u;
     }
-    a.w_lo = (uint32_t)c->window;
-    a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
-    for (int i = 0; i < c->nclass; ++i) a.rate[i] = ((class_mask >> i) & 1ull) ? c->crate_u64[i] : 0ull;
+    for (int i = 0; i < c->nclass; ++i) a.rate[i] = c->crate_u64[i];
     for (int j = 0; j < kLogTab; ++j) {   // log_spec tables, host libm
         a.log_c[j] = 128.0 / (double)(j + 91);
         a.log_l[j] = -std::log(a.log_c[j]);
@@ -314,6 +312,18 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     a.lcoef[3] = 0x1.5555555555555p-2;      // 1/3
     a.lcoef[4] = 0x1.62e42feep-1;           // ln2_hi (fdlibm)
     a.lcoef[5] = 0x1.a39ef35793c76p-33;     // ln2_lo (fdlibm)
+}
+
+kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull) {
+    SubstepArgs a = c->args;
+    a.plane0 = c->planes[0];                // (set_config swaps plane buffers)
+    a.plane1 = c->planes[1];
+    a.colour = colour;
+    a.D = D;
+    a.w_lo = (uint32_t)c->window;
+    a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
+    if (class_mask != ~0ull)
+        for (int i = 0; i < c->nclass; ++i) a.rate[i] = ((class_mask >> i) & 1ull) ? c->crate_u64[i] : 0ull;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         if (c->tev_used == c->tev.size()) {
@@ -601,6 +611,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     if (e != cudaSuccess) { kmc_destroy(c); return fail(nullptr, KMC_ECUDA, "init: %s", cudaGetErrorString(e)); }
 
     c->vgroup = vgroup;
+    build_args_template(c);
     if (world > 1 && !vgroup) {
         std::string why;
         if (!dist->nccl_unique_id) { kmc_destroy(c); return fail(nullptr, KMC_EINVAL, "world > 1 needs nccl_unique_id"); }
