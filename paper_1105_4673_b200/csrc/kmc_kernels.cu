@@ -86,7 +86,7 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     return L;
 }
 
-template <int KIND, int NDIM, int BS, int MINB, bool MH>
+template <int KIND, int NDIM, int BS, int MINB, bool MH, bool PF>
 __global__ void __launch_bounds__(BS, MINB)
 substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
     using M = Model<KIND, NDIM>;
@@ -156,7 +156,28 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         evsum += k;
     };
 
+    // PF: each lane also holds its NEXT cell, claimed and loaded one cell ahead, so the global-load
+    // latency of a refill overlaps the current cell's events instead of stalling the next step
+    uint32_t ni = 0, gidn = 0;
+    bool nhave = false;
+    uint64_t Pn[NP], hn[NP][4];
+    auto prefetch = [&](uint32_t c) {
+        const CellLoc L = locate<NDIM>(a, c);
+        gidn = L.gid32;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const uint64_t* pl = planes[p];
+            Pn[p] = pl[L.iC];
+            halo_from_words<MH>(g, pl[L.iW], pl[L.iE], NDIM == 2 ? pl[L.iN] : 0, NDIM == 2 ? pl[L.iS] : 0, hn[p], NDIM == 2);
+        }
+    };
     if (have) load(ci);
+    if (PF) {
+        ni = next + lane;
+        nhave = ni < cend;
+        if (nhave) prefetch(ni);
+        next += 32;
+    }
     // The event step is one branch-free basic block: lanes without a cell (queue exhausted) and
     // lanes whose window ended compute it too, with the update masked off, so the warp never
     // diverges inside the step and the scheduler can interleave its independent chains.
@@ -166,9 +187,26 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         if (fm) {                                                  // warp-uniform
             if (fin) {
                 store(ci);
-                ci = next + __popc(fm & ((1u << lane) - 1u));
-                have = ci < cend;
-                if (have) load(ci);
+                if (PF) {
+                    ci = ni;
+                    have = nhave;
+                    gid32 = gidn;
+                    k = 0;
+                    tclock = 0.0;
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        P[p] = Pn[p];
+#pragma unroll
+                        for (int d = 0; d < 4; ++d) h[p][d] = hn[p][d];
+                    }
+                    ni = next + __popc(fm & ((1u << lane) - 1u));
+                    nhave = ni < cend;
+                    if (nhave) prefetch(ni);
+                } else {
+                    ci = next + __popc(fm & ((1u << lane) - 1u));
+                    have = ci < cend;
+                    if (have) load(ci);
+                }
             }
             next += __popc(fm);
             if (!__any_sync(FULL, have)) break;
@@ -185,8 +223,11 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
     if (nactive <= 0) return cudaSuccess;
     // launch shape (block size, min blocks per SM): env KMC_LB selects an experiment variant
     static const int lb = [] { const char* e = getenv("KMC_LB"); return e ? atoi(e) : 0; }();
-    int bs = 256;
-    if (KIND == 0 && lb == 1 && a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2)) bs = 128;
+    static const int pf_env = [] { const char* e = getenv("KMC_PF"); return e ? atoi(e) : -1; }();
+    // next-cell prefetch: measured 2-12 % SLOWER on B200 (the extra registers cost occupancy and the
+    // refill loads are not the bottleneck), so it is off unless KMC_PF=1
+    const bool pf = pf_env == 1;
+    const int bs = 256;
     // cells per warp: 32 lanes x a few cells each, so a lane's tail idles for ~1/cpl of the window
     long long cpl = 8;
     while (cpl > 1 && (nactive + 32 * cpl - 1) / (32 * cpl) < 4 * 148 * 8) cpl >>= 1;   // keep >= ~4 waves
@@ -197,18 +238,22 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
     // merged halo boards need disjoint first/last columns (and rows in 2D)
     const bool mh = a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2);
     if constexpr (KIND == 0) {
-        // spin flip default: <= 80 registers, 3 blocks of 256 (24 warps) per SM
-        if (!mh) substep_kernel<KIND, NDIM, 256, 3, false><<<nb, 256, 0, s>>>(a, na, ch);
-        else if (lb == 1) substep_kernel<KIND, NDIM, 128, 5, true><<<nb, 128, 0, s>>>(a, na, ch);   // <= 96 regs
-        else if (lb == 3) substep_kernel<KIND, NDIM, 256, 2, true><<<nb, 256, 0, s>>>(a, na, ch);   // <= 128 regs
-        else substep_kernel<KIND, NDIM, 256, 3, true><<<nb, 256, 0, s>>>(a, na, ch);
+        // spin flip default: <= 80 registers (uses ~60-70), 256 threads, >= 3 CTAs per SM
+        if (!mh) substep_kernel<KIND, NDIM, 256, 3, false, false><<<nb, bs, 0, s>>>(a, na, ch);
+        else if (pf) substep_kernel<KIND, NDIM, 256, 3, true, true><<<nb, bs, 0, s>>>(a, na, ch);
+        else substep_kernel<KIND, NDIM, 256, 3, true, false><<<nb, bs, 0, s>>>(a, na, ch);
     } else {
         // hop / pair models need q >= 2 (R7), so the merged boards always apply.  Measured on B200:
         // diffusion (22 masks live) is fastest with <= 128 registers (2 CTAs/SM), ZGB (counts +
         // rebuilt mask) with <= 80 registers (3 CTAs/SM).  KMC_LB=3 forces 128, KMC_LB=4 forces 80.
         const bool big = (KIND == 1 && lb != 4) || lb == 3;
-        if (big) substep_kernel<KIND, NDIM, 256, 2, true><<<nb, 256, 0, s>>>(a, na, ch);
-        else substep_kernel<KIND, NDIM, 256, 3, true><<<nb, 256, 0, s>>>(a, na, ch);
+        if (big) {
+            if (pf) substep_kernel<KIND, NDIM, 256, 2, true, true><<<nb, bs, 0, s>>>(a, na, ch);
+            else substep_kernel<KIND, NDIM, 256, 2, true, false><<<nb, bs, 0, s>>>(a, na, ch);
+        } else {
+            if (pf) substep_kernel<KIND, NDIM, 256, 3, true, true><<<nb, bs, 0, s>>>(a, na, ch);
+            else substep_kernel<KIND, NDIM, 256, 3, true, false><<<nb, bs, 0, s>>>(a, na, ch);
+        }
     }
     return cudaGetLastError();
 }
