@@ -98,6 +98,17 @@ def cpu_baseline_sample(wl, seconds_hint="~10-30 s"):
                       f"macro-steps dt={wl['dt']}, {o.events} events in {el:.1f} s, 1 thread"}
 
 
+def arm_config(workload, dt, world):
+    """The `config` object of both arms (the workload the metric is quoted on)."""
+    wl = si.WORKLOADS[workload]
+    C = 2 if (wl["ndim"] == 1 or wl["kind"] == "adsdes") else 4
+    return {"workload": workload, "dims_per_gpu": list(wl["dims"]), "cell": list(wl["cell"]),
+            "model": wl["kind"], "params": wl["params"], "scheme": wl["scheme"], "dt": dt,
+            "init": f"Bernoulli({wl['init']})", "colours": C,
+            "l2": "inputs larger than L2 (bit-packed lattice 128 MiB/GPU at 32768^2 > 126 MB L2)",
+            "parallelism": f"slab{world}" if wl["ndim"] == 2 else f"replicas{world}"}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (O2), timed on this host, bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
@@ -108,12 +119,13 @@ def run_reference(args):
     side = 256
     o = FSKMC(wl["ndim"], (side, side), wl["cell"], wl["kind"], model_params(**wl["params"]), seed=7)
     o.set_config(si.bernoulli_lattice((1, side, side), wl["init"], seed=si.SEED_BASE + 1))
+    dt = args.dt if args.dt is not None else wl["dt"]
     for _ in range(args.warmup):
-        o.run(wl["dt"], wl["dt"], wl["scheme"])
+        o.run(dt, dt, wl["scheme"])
     e0 = o.events
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        o.run(wl["dt"], wl["dt"], wl["scheme"])
+        o.run(dt, dt, wl["scheme"])
         o.observables()
     el = time.perf_counter() - t0
     v = (o.events - e0) / el
@@ -122,7 +134,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
-        "data": "synthetic", "config": {"workload": args.workload + f" (sample {side}x{side})"},
+        "data": "synthetic",
+        "config": arm_config(args.workload, args.dt if args.dt is not None else wl["dt"], args.gpus),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -289,11 +302,7 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
         "data": "synthetic",
-        "config": {"workload": args.workload, "dims_per_gpu": list(wl["dims"]), "cell": list(wl["cell"]),
-                   "model": wl["kind"], "params": wl["params"], "scheme": wl["scheme"], "dt": dt,
-                   "init": f"Bernoulli({wl['init']})", "colours": C,
-                   "l2": "inputs larger than L2 (bit-packed lattice 128 MiB/GPU at 32768^2 > 126 MB L2)",
-                   "parallelism": f"slab{world}" if ndim == 2 else f"replicas{world}"},
+        "config": arm_config(args.workload, dt, world),
         "site_updates_per_s": site_updates,
         "events_per_step": events / args.steps,
         "roofline": roof,
