@@ -114,9 +114,11 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     unsigned long long evsum = 0;
 
     // a3: stage the closure (cell + one-site halo) of cell `ci` into registers
+    uint32_t iCcur = 0;                                             // word index of the current cell
     auto load = [&](uint32_t c) {
         const CellLoc L = locate<NDIM>(a, c);
         gid32 = L.gid32;
+        iCcur = L.iC;
         k = 0;
         tclock = 0.0;
 #pragma unroll
@@ -129,6 +131,12 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     // a6: write the cell back once per window (+ halo deltas for hop / pair events)
     auto store = [&](uint32_t c) {
         if (k == 0) return;
+        if constexpr (KIND == 0) {   // spin flip writes only its own word: no second locate
+            planes[0][iCcur] = P[0];
+            atomicAdd(&a.wev[iCcur - (uint32_t)g.ghost * ((uint32_t)g.R * g.Mx)], k);
+            evsum += k;
+            return;
+        }
         const CellLoc L = locate<NDIM>(a, c);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -158,12 +166,13 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
 
     // PF: each lane also holds its NEXT cell, claimed and loaded one cell ahead, so the global-load
     // latency of a refill overlaps the current cell's events instead of stalling the next step
-    uint32_t ni = 0, gidn = 0;
+    uint32_t ni = 0, gidn = 0, iCn = 0;
     bool nhave = false;
     uint64_t Pn[NP], hn[NP][4];
     auto prefetch = [&](uint32_t c) {
         const CellLoc L = locate<NDIM>(a, c);
         gidn = L.gid32;
+        iCn = L.iC;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const uint64_t* pl = planes[p];
@@ -191,6 +200,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
                     ci = ni;
                     have = nhave;
                     gid32 = gidn;
+                    iCcur = iCn;
                     k = 0;
                     tclock = 0.0;
 #pragma unroll
