@@ -108,6 +108,7 @@ struct kmc_ctx {
     long long plane_words = 0;
     uint32_t* wev = nullptr;
     unsigned long long* ev_total = nullptr;
+    unsigned int* queue = nullptr;           // window kernel's dynamic chunk counter
     unsigned long long* obs_buf = nullptr;   // kObsCounters + 1 (events)
     unsigned int* err_flag = nullptr;
     uint8_t* staging = nullptr;              // uint8 local slab (set/get_config from host)
@@ -291,6 +292,7 @@ void build_args_template(kmc_ctx* c) {
     a.g = c->g;
     a.wev = c->wev;
     a.ev_total = c->ev_total;
+    a.queue = c->queue;
     a.C = c->C;
     a.inv_scale = std::ldexp(1.0, -c->F);
     a.inv_half = 1.0 / (double)(c->g.Mx / 2);
@@ -595,6 +597,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     for (int p = 0; p < c->nplanes; ++p) ok = ok && alloc((void**)&c->planes[p], (size_t)c->plane_words * 8);
     ok = ok && alloc((void**)&c->wev, (size_t)owned * 4);
     ok = ok && alloc((void**)&c->ev_total, 8);
+    ok = ok && alloc((void**)&c->queue, 8);
     ok = ok && alloc((void**)&c->obs_buf, (kObsCounters + 1) * 8);
     ok = ok && alloc((void**)&c->err_flag, 4);
     if (g.ghost) {
@@ -633,7 +636,7 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
-    cudaFree(c->wev); cudaFree(c->ev_total); cudaFree(c->obs_buf); cudaFree(c->err_flag);
+    cudaFree(c->wev); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv);
     cudaFree(c->spare[0]); cudaFree(c->spare[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);

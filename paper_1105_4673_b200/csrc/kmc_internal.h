@@ -38,6 +38,7 @@ struct SubstepArgs {
     uint64_t* plane1;
     uint32_t* wev;                   // cumulative events per owned cell [My_local][R][Mx]
     unsigned long long* ev_total;    // device event counter
+    unsigned int* queue;             // dynamic chunk counter of the persistent window kernel
     int colour, C;
     double D;                        // window duration
     double inv_scale;                // 2^-F

@@ -86,7 +86,7 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     return L;
 }
 
-template <int KIND, int NDIM, int BS, int MINB, bool MH, bool PF>
+template <int KIND, int NDIM, int BS, int MINB, bool MH>
 __global__ void __launch_bounds__(BS, MINB)
 substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
     using M = Model<KIND, NDIM>;
@@ -98,23 +98,27 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) { s_logc[i] = a.log_c[i]; s_logl[i] = a.log_l[i]; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long cbeg64 = (unsigned long long)warp * chunk;
     if (cbeg64 >= nactive) return;                                  // warp-uniform
-    const uint32_t cbeg = (uint32_t)cbeg64;
-    const uint32_t cend = (uint32_t)min(cbeg64 + chunk, (unsigned long long)nactive);
+    // The grid is persistent (about one wave): warp w starts on chunk w, then claims further chunks
+    // of `chunk` cells from a global counter, so lanes never wait for a chunk boundary and there is
+    // no wave-quantisation tail -- lanes idle only in the kernel's last cell-times.
+    const unsigned long long pool0 = (unsigned long long)nwarps * chunk;   // first dynamic chunk
+    uint32_t next = (uint32_t)cbeg64 + 32;                           // warp-uniform queue head
+    uint32_t cend = (uint32_t)min(cbeg64 + chunk, (unsigned long long)nactive);
+    bool pool_open = pool0 < nactive;
     uint64_t* planes[2] = {a.plane0, a.plane1};
 
-    uint32_t next = cbeg + 32;                                      // warp-uniform queue head
-    uint32_t ci = cbeg + lane;
+    uint32_t ci = (uint32_t)cbeg64 + lane;
     bool have = ci < cend;
-    uint32_t gid32 = 0, k = 0;
+    uint32_t gid32 = 0, k = 0, iCcur = 0;
     double tclock = 0.0;
     uint64_t P[NP], h[NP][4];
     unsigned long long evsum = 0;
 
     // a3: stage the closure (cell + one-site halo) of cell `ci` into registers
-    uint32_t iCcur = 0;                                             // word index of the current cell
     auto load = [&](uint32_t c) {
         const CellLoc L = locate<NDIM>(a, c);
         gid32 = L.gid32;
@@ -164,29 +168,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         evsum += k;
     };
 
-    // PF: each lane also holds its NEXT cell, claimed and loaded one cell ahead, so the global-load
-    // latency of a refill overlaps the current cell's events instead of stalling the next step
-    uint32_t ni = 0, gidn = 0, iCn = 0;
-    bool nhave = false;
-    uint64_t Pn[NP], hn[NP][4];
-    auto prefetch = [&](uint32_t c) {
-        const CellLoc L = locate<NDIM>(a, c);
-        gidn = L.gid32;
-        iCn = L.iC;
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            const uint64_t* pl = planes[p];
-            Pn[p] = pl[L.iC];
-            halo_from_words<MH>(g, pl[L.iW], pl[L.iE], NDIM == 2 ? pl[L.iN] : 0, NDIM == 2 ? pl[L.iS] : 0, hn[p], NDIM == 2);
-        }
-    };
     if (have) load(ci);
-    if (PF) {
-        ni = next + lane;
-        nhave = ni < cend;
-        if (nhave) prefetch(ni);
-        next += 32;
-    }
     // The event step is one branch-free basic block: lanes without a cell (queue exhausted) and
     // lanes whose window ended compute it too, with the update masked off, so the warp never
     // diverges inside the step and the scheduler can interleave its independent chains.
@@ -194,31 +176,27 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         const bool fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logc, s_logl);
         const unsigned fm = __ballot_sync(FULL, fin);
         if (fm) {                                                  // warp-uniform
+            const uint32_t need = __popc(fm);
+            const uint32_t rank = __popc(fm & ((1u << lane) - 1u));
+            const uint32_t avail = cend > next ? cend - next : 0u;
+            uint32_t nb = 0, nend = 0;
+            bool claimed = false;
+            if (need > avail && pool_open) {                       // warp-uniform: claim a chunk
+                if (lane == 0) nb = atomicAdd(a.queue, chunk);
+                const unsigned long long base = pool0 + __shfl_sync(FULL, nb, 0);
+                claimed = base < nactive;
+                pool_open = claimed;
+                nb = (uint32_t)base;
+                nend = claimed ? (uint32_t)min(base + chunk, (unsigned long long)nactive) : 0u;
+            }
             if (fin) {
                 store(ci);
-                if (PF) {
-                    ci = ni;
-                    have = nhave;
-                    gid32 = gidn;
-                    iCcur = iCn;
-                    k = 0;
-                    tclock = 0.0;
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        P[p] = Pn[p];
-#pragma unroll
-                        for (int d = 0; d < 4; ++d) h[p][d] = hn[p][d];
-                    }
-                    ni = next + __popc(fm & ((1u << lane) - 1u));
-                    nhave = ni < cend;
-                    if (nhave) prefetch(ni);
-                } else {
-                    ci = next + __popc(fm & ((1u << lane) - 1u));
-                    have = ci < cend;
-                    if (have) load(ci);
-                }
+                if (rank < avail) { ci = next + rank; have = true; }
+                else { ci = nb + (rank - avail); have = claimed && ci < nend; }
+                if (have) load(ci);
             }
-            next += __popc(fm);
+            if (claimed) { next = nb + (need - avail); cend = nend; }
+            else next += need;
             if (!__any_sync(FULL, have)) break;
         }
     }
@@ -228,46 +206,43 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     if (lane == 0 && evsum) atomicAdd(a.ev_total, evsum);
 }
 
+// resident CTAs per SM of one kernel instantiation (cached)
+template <typename K>
+static int resident_ctas(K kernel, int bs) {
+    int dev = 0, nsm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, bs, 0) != cudaSuccess || per < 1) per = 1;
+    return per * nsm;
+}
+
 template <int KIND, int NDIM>
 static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
     if (nactive <= 0) return cudaSuccess;
-    // launch shape (block size, min blocks per SM): env KMC_LB selects an experiment variant
+    // launch shape experiments: KMC_LB=3 forces the 128-register build, KMC_LB=4 the 80-register one
     static const int lb = [] { const char* e = getenv("KMC_LB"); return e ? atoi(e) : 0; }();
-    static const int pf_env = [] { const char* e = getenv("KMC_PF"); return e ? atoi(e) : -1; }();
-    // next-cell prefetch: measured 2-12 % SLOWER on B200 (the extra registers cost occupancy and the
-    // refill loads are not the bottleneck), so it is off unless KMC_PF=1
-    const bool pf = pf_env == 1;
-    const int bs = 256;
-    // cells per warp: 32 lanes x a few cells each, so a lane's tail idles for ~1/cpl of the window
-    long long cpl = 8;
-    while (cpl > 1 && (nactive + 32 * cpl - 1) / (32 * cpl) < 4 * 148 * 8) cpl >>= 1;   // keep >= ~4 waves
-    const long long chunk = 32 * cpl;
-    const long long nwarps = (nactive + chunk - 1) / chunk;
-    const unsigned nb = (unsigned)((nwarps * 32 + bs - 1) / bs);
-    const uint32_t na = (uint32_t)nactive, ch = (uint32_t)chunk;
-    // merged halo boards need disjoint first/last columns (and rows in 2D)
     static const int mh_env = [] { const char* e = getenv("KMC_MH"); return e ? atoi(e) : -1; }();
-    // spin flip: the four separate (window-constant) halo boards save 8 logic ops per event and
-    // were measured 3 % faster at dt = 1 than the merged pair, so merged boards are opt-in there
+    constexpr int bs = 256;
+    // merged halo boards need disjoint first/last columns (and rows in 2D).  Spin flip: the four
+    // separate (window-constant) boards save 8 logic ops per event and measured 3 % faster at
+    // dt = 1, so merged boards are opt-in there (KMC_MH=1).
     const bool mh = a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2) && !(KIND == 0 && mh_env != 1);
-    if constexpr (KIND == 0) {
-        // spin flip default: <= 80 registers (uses ~60-70), 256 threads, >= 3 CTAs per SM
-        if (!mh) substep_kernel<KIND, NDIM, 256, 3, false, false><<<nb, bs, 0, s>>>(a, na, ch);
-        else if (pf) substep_kernel<KIND, NDIM, 256, 3, true, true><<<nb, bs, 0, s>>>(a, na, ch);
-        else substep_kernel<KIND, NDIM, 256, 3, true, false><<<nb, bs, 0, s>>>(a, na, ch);
-    } else {
-        // hop / pair models need q >= 2 (R7), so the merged boards always apply.  Measured on B200:
-        // diffusion (22 masks live) is fastest with <= 128 registers (2 CTAs/SM), ZGB (counts +
-        // rebuilt mask) with <= 80 registers (3 CTAs/SM).  KMC_LB=3 forces 128, KMC_LB=4 forces 80.
-        const bool big = (KIND == 1 && lb != 4) || lb == 3;
-        if (big) {
-            if (pf) substep_kernel<KIND, NDIM, 256, 2, true, true><<<nb, bs, 0, s>>>(a, na, ch);
-            else substep_kernel<KIND, NDIM, 256, 2, true, false><<<nb, bs, 0, s>>>(a, na, ch);
-        } else {
-            if (pf) substep_kernel<KIND, NDIM, 256, 3, true, true><<<nb, bs, 0, s>>>(a, na, ch);
-            else substep_kernel<KIND, NDIM, 256, 3, true, false><<<nb, bs, 0, s>>>(a, na, ch);
-        }
-    }
+    // hop / pair models: diffusion (22 masks live) is fastest with <= 128 registers (2 CTAs/SM),
+    // ZGB (counts + rebuilt mask) with <= 80 registers (3 CTAs/SM) -- measured on B200
+    const bool big = KIND != 0 && ((KIND == 1 && lb != 4) || lb == 3);
+    auto kern = KIND == 0 ? (mh ? substep_kernel<KIND, NDIM, bs, 3, true> : substep_kernel<KIND, NDIM, bs, 3, false>)
+                          : (big ? substep_kernel<KIND, NDIM, bs, 2, true> : substep_kernel<KIND, NDIM, bs, 3, true>);
+    // persistent grid: one wave of resident warps, each starting on its own chunk of 32*cpl cells
+    static int cap_q3 = 0, cap_q2 = 0, cap_nm = 0;
+    int& cap = KIND == 0 ? (mh ? cap_q3 : cap_nm) : (big ? cap_q2 : cap_q3);
+    if (cap == 0) cap = resident_ctas(kern, bs);
+    const long long chunk = 32 * 8;
+    const long long want = (nactive + chunk - 1) / chunk;          // warps if every warp took one chunk
+    const long long nwarps = want < (long long)cap * (bs / 32) ? want : (long long)cap * (bs / 32);
+    const unsigned nb = (unsigned)((nwarps * 32 + bs - 1) / bs);
+    cudaError_t e = cudaMemsetAsync(a.queue, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    kern<<<nb, bs, 0, s>>>(a, (uint32_t)nactive, (uint32_t)chunk);
     return cudaGetLastError();
 }
 
