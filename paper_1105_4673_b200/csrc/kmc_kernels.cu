@@ -230,11 +230,14 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
     // hop / pair models: diffusion (22 masks live) is fastest with <= 128 registers (2 CTAs/SM),
     // ZGB (counts + rebuilt mask) with <= 80 registers (3 CTAs/SM) -- measured on B200
     const bool big = KIND != 0 && ((KIND == 1 && lb != 4) || lb == 3);
-    auto kern = KIND == 0 ? (mh ? substep_kernel<KIND, NDIM, bs, 3, true> : substep_kernel<KIND, NDIM, bs, 3, false>)
+    // spin flip: <= 64 registers (61 used, no spills) -> 4 CTAs of 256 per SM; KMC_LB=6: <= 80
+    const bool four = KIND == 0 && !mh && lb != 6;
+    auto kern = KIND == 0 ? (mh ? substep_kernel<KIND, NDIM, bs, 3, true>
+                                : (four ? substep_kernel<KIND, NDIM, bs, 4, false> : substep_kernel<KIND, NDIM, bs, 3, false>))
                           : (big ? substep_kernel<KIND, NDIM, bs, 2, true> : substep_kernel<KIND, NDIM, bs, 3, true>);
     // persistent grid: one wave of resident warps, each starting on its own chunk of 32*cpl cells
-    static int cap_q3 = 0, cap_q2 = 0, cap_nm = 0;
-    int& cap = KIND == 0 ? (mh ? cap_q3 : cap_nm) : (big ? cap_q2 : cap_q3);
+    static int cap_q3 = 0, cap_q2 = 0, cap_nm = 0, cap_4 = 0;
+    int& cap = KIND == 0 ? (mh ? cap_q3 : (four ? cap_4 : cap_nm)) : (big ? cap_q2 : cap_q3);
     if (cap == 0) cap = resident_ctas(kern, bs);
     const long long chunk = 32 * 8;
     const long long want = (nactive + chunk - 1) / chunk;          // warps if every warp took one chunk
