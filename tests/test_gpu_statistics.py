@@ -220,3 +220,25 @@ def test_1d_two_point_correlation_vs_exact():
         m, se = s.mean(axis=0), s.std(axis=0, ddof=1) / math.sqrt(6)
         ex = np.array([exact.paper_corr1d_corrected(beta, K, hp, r) for r in range(11)])
         assert np.all(np.abs(m - ex) <= np.maximum(4 * se, 3e-3)), (beta, m - ex, se)
+
+
+def test_2d_correlation_long_range_order():
+    """eq.(exactcorr2d) (P:1090-1098): below T_c the spin correlation tends to (1 - kappa^2)^{1/4}
+    = M^2, i.e. for the lattice gas E[s_0 s_r] -> c^2 with c from eq.(exactcov2d) (beta = 3,
+    kappa = sinh(beta K/2)^-2 ~ 0.021 so the O(kappa^r) term is gone by r = 4)."""
+    kmc = _kmc()
+    beta = 3.0
+    g = kmc.KMC(2, (256, 256), (8, 8), kind="adsdes", seed=4, ca=1.0, cd=1.0, beta=beta, K=1.0, h=-2.0)
+    g.set_config(np.ones(g.local_shape, np.uint8))
+    g.run(100.0, 1.0, "lie")
+    acc = np.zeros((2, 33))
+    for _ in range(20):
+        g.run(2.0, 1.0, "lie")
+        c = g.correlation(32)
+        acc += np.array([c["x"], c["y"]]) / (256 * 256)
+    acc /= 20
+    c2 = exact.paper_cov2d(beta, 1.0) ** 2
+    kappa = math.sinh(0.5 * beta) ** -2
+    assert abs((1 - kappa ** 2) ** 0.25 - (2 * exact.paper_cov2d(beta, 1.0) - 1) ** 2) < 1e-12   # M^2 identity
+    assert np.all(np.abs(acc[:, 4:] - c2) < 3e-3), (acc[:, 4:] - c2).max()
+    assert np.allclose(acc[:, 0], exact.paper_cov2d(beta, 1.0), atol=3e-3)                       # r = 0: coverage
