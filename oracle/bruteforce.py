@@ -182,6 +182,42 @@ def law_sequence(p0, Qc, seq):
     return p
 
 
+class NestedLattice(Lattice):
+    """f3 (eq.(sublatt2), R28): the cell partition of Lattice, grouped into outer
+    blocks of `block` cells along the last cell axis of the lattice (cell rows in 2D, cells in
+    1D) coloured by block parity.  colour(i) = outer * C + cell colour, so generators() returns
+    the 2C generators L^{o,c} of eq.(opdecomp2), indexed o*C + c."""
+
+    def __init__(self, ndim, H, W, qy, qx, C, block):
+        super().__init__(ndim, H, W, qy, qx, C)
+        self.C_cell, self.block = C, block
+        self.C = 2 * C
+
+    def colour(self, i):
+        y, x = divmod(i, self.W)
+        cy, cx = y // self.qy, x // self.qx
+        if self.C_cell == 2:
+            c = cx % 2 if self.ndim == 1 else (cx + cy) % 2
+        else:
+            c = cx % 2 + 2 * (cy % 2)
+        o = ((cy if self.ndim == 2 else cx) // self.block) % 2
+        return o * self.C_cell + c
+
+
+def law_nested(p0, Qc2, C, dt, T, n_inner, outer, inner):
+    """Exact law of the nested scheme (R28) with a deterministic inner scheme: per macro-step the
+    outer Lie [(0,dt),(1,dt)] or Strang [(0,dt/2),(1,dt),(0,dt/2)] factors, each split into
+    n_inner cycles of `inner` ('lie' / 'strang') over the C cell colours; Qc2[o*C + c]."""
+    outer_list = [(0, dt), (1, dt)] if outer == "lie" else [(0, dt / 2), (1, dt), (0, dt / 2)]
+    p = p0.copy()
+    for _ in range(int(round(T / dt))):
+        for o, Do in outer_list:
+            for _k in range(n_inner):
+                for c, d in _inner(inner, C, Do / n_inner):
+                    p = evolve(p, Qc2[o * C + c], d)
+    return p
+
+
 def coverage_values(lat, S, state=1, sites=None):
     """Per-configuration coverage of `state` (fraction of `sites`, default all)."""
     N = lat.N

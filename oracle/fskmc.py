@@ -101,6 +101,31 @@ def substeps(scheme: int, C: int, d: float, seed: int, w0: int):
     raise ValueError("unknown scheme")
 
 
+def nested_substeps(outer: int, inner: int, C: int, d: float, n_inner: int, seed: int, w0: int):
+    """f3, R28: the windows (outer colour o, cell colour c, duration) of ONE nested macro-step.
+
+    Outer factor list over the two outer colours (eq.(opdecomp) on the outer blocks):
+      Lie [(0, d), (1, d)];  Strang [(0, d/2), (1, d), (0, d/2)].
+    Each outer factor e^{D L^o} is itself split by eq.(opdecomp2): n_inner cycles of
+    the inner scheme over the C cell colours of duration D/n_inner each.  Window ids are consumed
+    in list order from w0 (the random inner scheme draws xi_w by those ids, R4)."""
+    if outer == LIE:
+        outer_list = [(0, d), (1, d)]
+    elif outer == STRANG:
+        outer_list = [(0, d * 0.5), (1, d), (0, d * 0.5)]
+    else:
+        raise ValueError("nested outer scheme must be lie or strang")
+    out = []
+    w = w0
+    for o, Do in outer_list:
+        di = Do / n_inner
+        for _ in range(n_inner):
+            for c, D in substeps(inner, C, di, seed, w):
+                out.append((o, c, D))
+                w += 1
+    return out
+
+
 class FSKMC:
     """O2: fractional-step KMC on a uint8 site-major lattice [R][H][W], periodic."""
 
@@ -216,6 +241,46 @@ class FSKMC:
             for dur, cls in [(h, slow)] + [(df, fast)] * n_fast + [(h, slow)]:
                 for colour, D in substeps(sc, self.C, dur, self.seed, self.window):
                     self.substep(colour, D, cls)
+            self.time += d
+        return truncated
+
+    def nested_cells(self, outer_colour: int, colour: int, block: int):
+        """Cells (replica, cy, cx) of cell colour `colour` inside the outer blocks of colour
+        `outer_colour` (R28): outer block = cell row // block (2D) or cell // block (1D), outer
+        colour = block index mod 2."""
+        r, cy, cx = np.meshgrid(np.arange(self.R), np.arange(self.My), np.arange(self.Mx), indexing="ij")
+        ob = (cy if self.ndim == 2 else cx) // block
+        if self.C == 2:
+            col = cx % 2 if self.ndim == 1 else (cx + cy) % 2
+        else:
+            col = cx % 2 + 2 * (cy % 2)
+        sel = (ob % 2 == outer_colour) & (col == colour)
+        return np.stack([r[sel], cy[sel], cx[sel]], axis=1).astype(np.int64)
+
+    def run_nested(self, T: float, dt: float, n_inner: int, outer="lie", inner="lie", block=2) -> bool:
+        """f3, eq.(sublatt2)/eq.(opdecomp2), R28: per macro-step d the outer scheme
+        over the two outer block colours, each outer factor split into n_inner cycles of the inner
+        scheme over the cell colours (nested_substeps); one window per (outer, cell colour)."""
+        so = SCHEME[outer] if isinstance(outer, str) else int(outer)
+        si = SCHEME[inner] if isinstance(inner, str) else int(inner)
+        n_inner = int(n_inner)
+        block = int(block)
+        nb = self.My if self.ndim == 2 else self.Mx
+        if n_inner < 1 or block < 2 or block % 2 or nb % (2 * block):
+            raise ValueError("nested: need n_inner >= 1, even block >= 2, cells per axis % (2 block) == 0")
+        durs, truncated = macro_steps(T, dt)
+        cache = {}
+        M = self.Mx * self.My
+        for d in durs:
+            for o, c, D in nested_substeps(so, si, self.C, d, n_inner, self.seed, self.window):
+                if (o, c) not in cache:
+                    cache[(o, c)] = self.nested_cells(o, c, block)
+                cells = cache[(o, c)]
+                ev = self.window_cells(cells, D, self.window)
+                gid = cells[:, 0] * M + cells[:, 1] * self.Mx + cells[:, 2]
+                self.W_events[gid] += ev
+                self.events += int(ev.sum())
+                self.window += 1
             self.time += d
         return truncated
 

@@ -209,3 +209,55 @@ def test_multiscale_generator_split_and_order():
     ex = bf.law(p0, Q, Qc, "exact", 0, 1.0, 2) @ cov
     e = [abs(bf.law_multiscale(p0, Qsc, Qfc, dt, 1.0, 3, "strang", 2) @ cov - ex) for dt in (0.25, 0.125)]
     assert 3.0 < e[0] / e[1] < 5.5, e
+
+
+def test_nested_generator_split_and_inner_order():
+    """f3 (eq.(sublatt2), eq.(opdecomp2), R28): the 2C nested generators L^{o,c} sum
+    to L and, over o, to each cell-colour generator L^c; as n_inner grows the nested scheme
+    converges to the outer scheme with EXACT outer factors e^{D L^o}, at second order with a
+    Strang inner scheme and first order with Lie (ratios 4 and -> 2 per doubling of n_inner)."""
+    m = ising(beta=1.0, K=1.0, h=-1.0)
+    lat = bf.Lattice(1, 1, 8, 1, 1, 2)
+    nl = bf.NestedLattice(1, 1, 8, 1, 1, 2, 2)
+    Q, Qc, S = bf.generators(m, lat)
+    Q2, Qc2, _ = bf.generators(m, nl)
+    assert len(Qc2) == 4
+    assert abs(Q - Q2).max() < 1e-12
+    for c in range(2):
+        assert abs(Qc[c] - Qc2[c] - Qc2[2 + c]).max() < 1e-12
+    # cell 0 (x = 0) is in outer block 0, cell colour 0; cell 2 in outer block 1
+    assert nl.colour(0) == 0 and nl.colour(1) == 1 and nl.colour(2) == 2 and nl.colour(3) == 3
+    p0 = bf.point_mass(S, 8, [1, 1, 0, 0, 1, 0, 0, 1])
+    cov = bf.coverage_values(lat, S, sites=[0, 1])
+    QE, QO = Qc2[0] + Qc2[1], Qc2[2] + Qc2[3]
+    dt, T = 0.5, 1.0
+    for outer, seq in (("lie", [(0, dt), (1, dt)]), ("strang", [(0, dt / 2), (1, dt), (0, dt / 2)])):
+        p = p0.copy()
+        for _ in range(2):
+            for o, d in seq:
+                p = bf.evolve(p, [QE, QO][o], d)
+        ref = p @ cov
+        es = [abs(bf.law_nested(p0, Qc2, 2, dt, T, n, outer, "strang") @ cov - ref) for n in (2, 4, 8)]
+        el = [abs(bf.law_nested(p0, Qc2, 2, dt, T, n, outer, "lie") @ cov - ref) for n in (4, 8)]
+        assert 3.8 < es[0] / es[1] < 4.2 and 3.8 < es[1] / es[2] < 4.2, (outer, es)
+        assert 1.9 < el[0] / el[1] < 2.9, (outer, el)
+
+
+def test_nested_noninteracting_exact_and_gibbs_invariance():
+    """K = 0: all nested generators commute, so the nested scheme is exact (closed form theta);
+    spin flip: pi L^{o,c} = 0 for each of the 2C nested generators (detailed balance, R9)."""
+    nl = bf.NestedLattice(1, 1, 8, 1, 1, 2, 2)
+    m0 = ising(beta=1.0, K=0.0, h=0.3, ca=1.0, cd=0.5)
+    Q, Qc2, S = bf.generators(m0, nl)
+    p0 = bf.point_mass(S, 8, [0] * 8)
+    cov = bf.coverage_values(nl, S)
+    th = exact.noninteracting_theta(1.5, 1.0, 0.5, 1.0, 0.3)
+    for outer, inner, n in (("lie", "lie", 1), ("lie", "strang", 3), ("strang", "lie", 2)):
+        assert abs(bf.law_nested(p0, Qc2, 2, 0.5, 1.5, n, outer, inner) @ cov - th) < 1e-9
+    m = ising(beta=1.3, K=1.0, h=-0.4, ca=1.0, cd=0.7)
+    Q, Qc2, S = bf.generators(m, nl)
+    w, v = np.linalg.eig(Q.toarray().T)
+    pi = np.real(v[:, np.argmin(np.abs(w))])
+    pi = pi / pi.sum()
+    for Qk in Qc2:
+        assert np.abs(pi @ Qk.toarray()).max() < 1e-12

@@ -210,3 +210,21 @@ def test_o2_multiscale_law(inner):
     sim.set_config(np.broadcast_to(start, (R, 1, N)))
     sim.run_multiscale(T, dt, nf, inner)
     check_law(confs_index(sim.get_config(), S), law)
+
+
+@pytest.mark.parametrize("outer,inner,n_inner", [("lie", "lie", 2), ("strang", "strang", 2), ("lie", "strang", 1)])
+def test_o2_nested_law(outer, inner, n_inner):
+    """f3: O2's nested scheme (eq.(opdecomp2), R28) samples the brute-force law exactly
+    (1D ring of 8 single-site cells, outer blocks of 2 cells)."""
+    N, q, dt, T, R, B = 8, 1, 0.5, 1.0, 20000, 2
+    p = dict(ca=1.0, cd=1.0, beta=1.0, K=1.0, h=-1.0)
+    nl = bf.NestedLattice(1, 1, N, 1, q, 2, B)
+    Q, Qc2, S = bf.generators(bf_model("adsdes", p), nl)
+    start = np.array([1, 1, 0, 0, 1, 0, 0, 1], np.uint8)
+    law = bf.law_nested(bf.point_mass(S, N, start), Qc2, 2, dt, T, n_inner, outer, inner)
+    sim = FSKMC(1, (N,), (q,), "adsdes", model_params(**p), colours=2, replicas=R, seed=41)
+    sim.set_config(np.broadcast_to(start, (R, 1, N)))
+    sim.run_nested(T, dt, n_inner, outer, inner, B)
+    check_law(confs_index(sim.get_config(), S), law)
+    assert sim.window == 2 * (len(bf._inner(inner, 2, 1.0)) * n_inner * (2 if outer == "lie" else 3))
+    assert int(sim.W_events.sum()) == sim.events
