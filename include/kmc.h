@@ -139,6 +139,19 @@ kmc_status kmc_run(kmc_ctx* ctx, double T, double dt, kmc_scheme scheme);
 kmc_status kmc_run_multiscale(kmc_ctx* ctx, double T, double dt, int32_t n_fast, kmc_scheme inner,
                               uint64_t fast_classes);
 
+/* Nested two-level decomposition (eq.(sublatt2), eq.(opdecomp2), P:841-855;
+ * DESIGN.md R28).  Outer blocks = `block` consecutive cell rows (2D; cells in 1D), coloured by block
+ * parity (the paper's C_m^E / C_m^O); the cells inside are the paper's D_ml.  Per macro-step d the
+ * outer Lie (0,d)(1,d) or Strang (0,d/2)(1,d)(0,d/2) factors; each outer factor of duration D is
+ * n_inner cycles of the `inner` scheme (Lie, Strang, random) over the C cell colours, of duration
+ * D/n_inner, restricted to the blocks of that outer colour.  With world > 1 the halo exchange runs
+ * once per OUTER factor instead of once per window (blocks may not straddle ranks).  Errors:
+ * KMC_EINVAL for outer = random, n_inner < 1, or an odd block / block < 2; KMC_EPARTITION when the
+ * cells per axis are not a multiple of 2*block, or (world > 1) the local cell rows not a multiple
+ * of block; KMC_WTRUNCATED as kmc_run.  Asynchronous. */
+kmc_status kmc_run_nested(kmc_ctx* ctx, double T, double dt, int32_t n_inner, kmc_scheme outer, kmc_scheme inner,
+                          int32_t block);
+
 /* One window: every cell of colour `colour` runs its SSA for `duration` (eq.(exact)); the window
  * counter advances by one, physical time does not.  Asynchronous. */
 kmc_status kmc_substep(kmc_ctx* ctx, int32_t colour, double duration);
@@ -171,7 +184,8 @@ kmc_status kmc_rate_table(const kmc_ctx* ctx, int32_t* n, int32_t* type, int32_t
  *   KMC_KERNEL_QUEUE: lane-per-cell kernel, per-warp cell queues, closure loaded from global memory;
  *   KMC_KERNEL_TILE:  2D spin-flip only -- a CTA stages a 32x64-cell tile + halo in shared memory and
  *                     runs its active cells from a CTA queue (best when a window holds few events);
- *   KMC_KERNEL_AUTO:  tile when D x sites x mean class rate < 16, else queue (env KMC_TILE=0/1 overrides).
+ *   KMC_KERNEL_AUTO:  queue (measured faster in every regime on B200; env KMC_TILE=0/1 overrides).
+ * Nested windows (kmc_run_nested) always use the queue kernel.
  * KMC_EINVAL for an unknown mode. */
 typedef enum { KMC_KERNEL_AUTO = 0, KMC_KERNEL_QUEUE = 1, KMC_KERNEL_TILE = 2 } kmc_kernel_mode;
 kmc_status kmc_set_kernel(kmc_ctx* ctx, int32_t mode);
@@ -198,6 +212,9 @@ kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, i
                              void* stream, kmc_ctx** out);
 kmc_status kmc_vgroup_run(kmc_ctx** ctxs, int32_t world, double T, double dt, kmc_scheme scheme);
 kmc_status kmc_vgroup_sync(kmc_ctx** ctxs, int32_t world);
+/* kmc_run_nested on a virtual-rank group (one exchange per outer factor). */
+kmc_status kmc_vgroup_run_nested(kmc_ctx** ctxs, int32_t world, double T, double dt, int32_t n_inner,
+                                 kmc_scheme outer, kmc_scheme inner, int32_t block);
 
 /* NCCL unique id for world > 1 (rank 0 calls it and broadcasts the 128 bytes). */
 kmc_status kmc_nccl_unique_id(uint8_t out[128]);

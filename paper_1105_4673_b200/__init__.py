@@ -27,7 +27,8 @@ EXPORTS = [
     "kmc_run", "kmc_substep", "kmc_observables", "kmc_get_state", "kmc_set_state",
     "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
     "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
-    "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale",
+    "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale", "kmc_run_nested",
+    "kmc_vgroup_run_nested",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -101,6 +102,8 @@ def lib():
         "kmc_set_kernel": ([vp, i32], i32),
         "kmc_correlation": ([vp, i32, i32, vp, vp], i32),
         "kmc_run_multiscale": ([vp, dbl, dbl, i32, i32, u64], i32),
+        "kmc_run_nested": ([vp, dbl, dbl, i32, i32, i32, i32], i32),
+        "kmc_vgroup_run_nested": ([vp, i32, dbl, dbl, i32, i32, i32, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -230,6 +233,16 @@ class KMC:
                                                     int(fast_classes)), allow=(KMC_WTRUNCATED,))
         return st == KMC_WTRUNCATED
 
+    def run_nested(self, T, dt, n_inner, outer="lie", inner="lie", block=2):
+        """kmc_run_nested (f3, eq.(opdecomp2), R28): outer Lie/Strang over the two outer block
+        colours, each outer factor n_inner cycles of `inner` over the cell colours; returns the
+        truncation flag."""
+        so = SCHEMES[outer] if isinstance(outer, str) else int(outer)
+        si = SCHEMES[inner] if isinstance(inner, str) else int(inner)
+        st = self._check(self._L.kmc_run_nested(self._ctx, float(T), float(dt), int(n_inner), so, si,
+                                                int(block)), allow=(KMC_WTRUNCATED,))
+        return st == KMC_WTRUNCATED
+
     def substep(self, colour, duration):
         self._check(self._L.kmc_substep(self._ctx, int(colour), float(duration)))
 
@@ -351,6 +364,13 @@ class VGroup:
     def run(self, T, dt, scheme="lie"):
         sc = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
         return self._check(self._L.kmc_vgroup_run(self._arr, self.world, float(T), float(dt), sc),
+                           allow=(KMC_WTRUNCATED,)) == KMC_WTRUNCATED
+
+    def run_nested(self, T, dt, n_inner, outer="lie", inner="lie", block=2):
+        so = SCHEMES[outer] if isinstance(outer, str) else int(outer)
+        si = SCHEMES[inner] if isinstance(inner, str) else int(inner)
+        return self._check(self._L.kmc_vgroup_run_nested(self._arr, self.world, float(T), float(dt), int(n_inner),
+                                                         so, si, int(block)),
                            allow=(KMC_WTRUNCATED,)) == KMC_WTRUNCATED
 
     def observables(self):

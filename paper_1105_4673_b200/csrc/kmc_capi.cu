@@ -295,7 +295,8 @@ void build_args_template(kmc_ctx* c) {
     a.queue = c->queue;
     a.C = c->C;
     a.inv_scale = std::ldexp(1.0, -c->F);
-    a.inv_half = 1.0 / (double)(c->g.Mx / 2);
+    a.half = (uint32_t)(c->g.Mx / 2);
+    a.inv_half = 1.0 / (double)a.half;
     a.inv_R = 1.0 / (double)c->g.R;
     a.key0 = (uint32_t)c->geom.seed;
     a.key1 = (uint32_t)(c->geom.seed >> 32);
@@ -316,12 +317,41 @@ void build_args_template(kmc_ctx* c) {
     a.lcoef[5] = 0x1.a39ef35793c76p-33;     // ln2_lo (fdlibm)
 }
 
-kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull) {
+// f3 nested decomposition (R28): restrict a window to the outer blocks of one outer colour.
+struct Nest {
+    int outer;    // outer colour 0/1
+    int block;    // outer block size in cell rows (2D) or cells (1D)
+};
+
+// Fills the nested fields of the kernel arguments; returns the number of active cells.
+long long apply_nest(const kmc_ctx* c, const Nest& n, SubstepArgs& a) {
+    const long long half = c->g.Mx / 2;
+    a.nest = 1;
+    a.nest_B = n.block;
+    if (c->g.ndim == 1) {              // blocks of B cells along x; B/2 colour pairs per block
+        const long long nblk = c->g.Mx / n.block;
+        a.nest_s = n.outer;
+        a.nest_rows = (uint32_t)(n.block / 2);
+        a.half = (uint32_t)((nblk / 2) * (n.block / 2));
+        a.inv_half = 1.0 / (double)a.half;
+        a.inv_nest_rows = 1.0 / (double)a.nest_rows;
+        return (long long)a.half * c->g.R;
+    }
+    const int nblk_loc = c->g.My_local / n.block;
+    a.nest_s = (n.outer + c->g.row_offset / n.block) & 1;   // local block 0 is global block row_offset/B
+    const int n_o = (nblk_loc - a.nest_s + 1) / 2;           // local blocks of this outer colour
+    a.nest_rows = (uint32_t)(c->C == 2 ? n.block : n.block / 2);
+    a.inv_nest_rows = 1.0 / (double)a.nest_rows;
+    return half * c->g.R * (long long)n_o * a.nest_rows;
+}
+
+kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull, const Nest* nest = nullptr) {
     SubstepArgs a = c->args;
     a.plane0 = c->planes[0];                // (set_config swaps plane buffers)
     a.plane1 = c->planes[1];
     a.colour = colour;
     a.D = D;
+    const long long nactive = nest ? apply_nest(c, *nest, a) : active_cells(c);
     a.w_lo = (uint32_t)c->window;
     a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
     if (class_mask != ~0ull)
@@ -344,12 +374,12 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     static const int tile_env = [] { const char* e = getenv("KMC_TILE"); return e ? atoi(e) : -1; }();
     int mode = c->kernel_mode;                                   // kmc_set_kernel: 0 auto, 1 queue, 2 tile
     if (mode == KMC_KERNEL_AUTO && tile_env >= 0) mode = tile_env ? KMC_KERNEL_TILE : KMC_KERNEL_QUEUE;
-    bool use_tile = c->kind == KMC_ADSDES && c->g.ndim == 2 && mode != KMC_KERNEL_QUEUE;
+    bool use_tile = c->kind == KMC_ADSDES && c->g.ndim == 2 && mode != KMC_KERNEL_QUEUE && !nest;
     // auto = queue: measured on B200 the tile kernel is 4-17 % slower at dt = 1 and dt = 0.01 (both
     // regimes are instruction-issue bound, not load-latency bound); it stays selectable
     if (use_tile && mode == KMC_KERNEL_AUTO) use_tile = false;
     cudaError_t le = use_tile ? launch_substep_tile(a, c->stream) : cudaErrorNotSupported;
-    if (le == cudaErrorNotSupported) le = launch_substep(c->kind, a, active_cells(c), c->stream);
+    if (le == cudaErrorNotSupported) le = launch_substep(c->kind, a, nactive, c->stream);
     CUDA_TRY(c, le);
     if (c->timing) CUDA_TRY(c, cudaEventRecord(e1, c->stream));
     c->window += 1;
@@ -400,6 +430,31 @@ std::vector<double> macro_durations(double T, double dt, bool* truncated) {
     out.assign((size_t)n, dt);
     out.back() = last;
     return out;
+}
+
+// f3 (R28): validation of a nested run and its outer factor list for one macro-step d.
+kmc_status check_nested(kmc_ctx* c, double T, double dt, int n_inner, int outer, int inner, int block) {
+    if (!(dt > 0.0) || !(T >= 0.0) || std::isinf(T)) return fail(c, KMC_EINVAL, "need dt > 0 and finite T >= 0");
+    if (outer != KMC_LIE && outer != KMC_STRANG) return fail(c, KMC_EINVAL, "nested outer scheme must be Lie or Strang");
+    if (inner < KMC_LIE || inner > KMC_RANDOM) return fail(c, KMC_EINVAL, "unknown inner scheme %d", inner);
+    if (n_inner < 1) return fail(c, KMC_EINVAL, "n_inner must be >= 1");
+    if (block < 2 || block % 2) return fail(c, KMC_EINVAL, "nested block must be even and >= 2");
+    if (c->g.ndim == 1) {
+        if (c->g.Mx % (2 * block)) return fail(c, KMC_EPARTITION, "nested: %d cells not a multiple of 2*block", c->g.Mx);
+    } else {
+        const long long rows = (long long)c->g.My_local * c->world;
+        if (rows % (2 * block)) return fail(c, KMC_EPARTITION, "nested: %lld cell rows not a multiple of 2*block", rows);
+        // outer blocks must not straddle ranks: then a rank's ghost rows belong to the other outer
+        // colour for a whole outer factor, and one exchange per outer factor suffices
+        if (c->world > 1 && c->g.My_local % block)
+            return fail(c, KMC_EPARTITION, "nested: %d local cell rows not a multiple of block", c->g.My_local);
+    }
+    return KMC_OK;
+}
+
+std::vector<std::pair<int, double>> outer_factors(int outer, double d) {
+    if (outer == KMC_LIE) return {{0, d}, {1, d}};
+    return {{0, d * 0.5}, {1, d}, {0, d * 0.5}};
 }
 
 // ---- virtual ranks: G slabs of one lattice on one device, exchanged by stream-ordered copies ----
@@ -782,6 +837,33 @@ kmc_status kmc_run_multiscale(kmc_ctx* c, double T, double dt, int32_t n_fast, k
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
 
+kmc_status kmc_run_nested(kmc_ctx* c, double T, double dt, int32_t n_inner, kmc_scheme outer, kmc_scheme inner,
+                          int32_t block) {
+    if (!c) return KMC_EINVAL;
+    if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: use kmc_vgroup_run_nested");
+    kmc_status st = check_nested(c, T, dt, n_inner, outer, inner, block);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    bool truncated = false;
+    for (double d : macro_durations(T, dt, &truncated)) {
+        for (const auto& of : outer_factors(outer, d)) {
+            // eq.(opdecomp2): e^{D L^o} ~ [inner cycle of duration D/n]^n.  One halo exchange per
+            // outer factor: the ghost rows belong to the inactive outer colour throughout it.
+            const Nest nest{of.first, block};
+            st = exchange_forward(c);
+            for (int k = 0; k < n_inner && st == KMC_OK; ++k)
+                for (const auto& sd : macro_schedule(inner, c->C, of.second / (double)n_inner, c->geom.seed, c->window)) {
+                    st = launch_window(c, sd.first, sd.second, ~0ull, &nest);
+                    if (st != KMC_OK) break;
+                }
+            if (st == KMC_OK) st = exchange_reverse(c);
+            if (st != KMC_OK) return st;
+        }
+        c->time += d;
+    }
+    return truncated ? KMC_WTRUNCATED : KMC_OK;
+}
+
 kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, int32_t world, int32_t device,
                              void* stream, kmc_ctx** out) {
     if (!geom || !model || !out || world < 2) return fail(nullptr, KMC_EINVAL, "vgroup needs world >= 2");
@@ -834,6 +916,34 @@ kmc_status kmc_vgroup_run(kmc_ctx** cs, int32_t world, double T, double dt, kmc_
         for (const auto& sd : macro_schedule(scheme, c0->C, d, c0->geom.seed, c0->window)) {
             kmc_status st = vgroup_forward(cs, world);
             for (int r = 0; r < world && st == KMC_OK; ++r) st = launch_window(cs[r], sd.first, sd.second);
+            if (st == KMC_OK) st = vgroup_reverse(cs, world);
+            if (st != KMC_OK) return st;
+        }
+        for (int r = 0; r < world; ++r) cs[r]->time += d;
+    }
+    return truncated ? KMC_WTRUNCATED : KMC_OK;
+}
+
+kmc_status kmc_vgroup_run_nested(kmc_ctx** cs, int32_t world, double T, double dt, int32_t n_inner,
+                                 kmc_scheme outer, kmc_scheme inner, int32_t block) {
+    if (!cs || world < 2) return KMC_EINVAL;
+    kmc_ctx* c0 = cs[0];
+    for (int r = 0; r < world; ++r)
+        if (!cs[r] || !cs[r]->vgroup || cs[r]->world != world || cs[r]->rank != r)
+            return fail(c0, KMC_EINVAL, "vgroup: contexts must be ranks 0..world-1 of one kmc_vgroup_create");
+    kmc_status st = check_nested(c0, T, dt, n_inner, outer, inner, block);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c0, cudaSetDevice(c0->device));
+    bool truncated = false;
+    for (double d : macro_durations(T, dt, &truncated)) {
+        for (const auto& of : outer_factors(outer, d)) {
+            const Nest nest{of.first, block};
+            st = vgroup_forward(cs, world);
+            for (int k = 0; k < n_inner && st == KMC_OK; ++k)
+                for (const auto& sd : macro_schedule(inner, c0->C, of.second / (double)n_inner, c0->geom.seed, c0->window)) {
+                    for (int r = 0; r < world && st == KMC_OK; ++r) st = launch_window(cs[r], sd.first, sd.second, ~0ull, &nest);
+                    if (st != KMC_OK) break;
+                }
             if (st == KMC_OK) st = vgroup_reverse(cs, world);
             if (st != KMC_OK) return st;
         }

@@ -42,7 +42,15 @@ struct SubstepArgs {
     int colour, C;
     double D;                        // window duration
     double inv_scale;                // 2^-F
-    double inv_half, inv_R;          // 1/(Mx/2), 1/R for fast_divmod in the cell locator
+    double inv_half, inv_R;          // 1/half, 1/R for fast_divmod in the cell locator
+    uint32_t half;                   // active cells per (row, replica): Mx/2, or the nested count in 1D
+    // f3 nested decomposition (R28): the window runs only the cells of the outer blocks (`nest_B`
+    // cell rows in 2D, cells in 1D) of one outer colour.  nest = 0: off.  In 2D the active rows are
+    // numbered block by block, nest_rows per block; nest_s = parity of the first local block
+    // that is active.
+    int nest, nest_B, nest_s;
+    uint32_t nest_rows;
+    double inv_nest_rows;
     uint32_t key0, key1;             // Philox key = seed
     uint32_t rk0[10], rk1[10];       // Philox round keys k + i*(W0, W1), i = 0..9 (warp-uniform)
     uint32_t w_lo, w_hi_tag;         // window id (tag EVT = 0 in bits 28..31)

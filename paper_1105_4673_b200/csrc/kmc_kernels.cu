@@ -43,24 +43,38 @@ struct CellLoc {
 
 // Active-cell number t -> cell location.  All indices fit 32 bits (kmc_create enforces < 2^32
 // cells in total, and a plane holds at most that many words plus two ghost rows).
-template <int NDIM>
+template <int NDIM, bool NEST>
 __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     const Geo& g = a.g;
-    const uint32_t half = (uint32_t)g.Mx >> 1;
     uint32_t rest, j, rowsel, r;
-    fast_divmod(t, half, a.inv_half, rest, j);
+    fast_divmod(t, a.half, a.inv_half, rest, j);
     if (g.R == 1) { rowsel = rest; r = 0; }
     else fast_divmod(rest, (uint32_t)g.R, a.inv_R, rowsel, r);
     uint32_t cy, cx;
     if (NDIM == 1) {
         cy = 0;
-        cx = 2 * j + a.colour;
-    } else if (a.C == 2) {
-        cy = rowsel;
-        cx = 2 * j + ((a.colour + g.row_offset + cy) & 1);
+        if (NEST) {               // f3: pair j of the active outer blocks (B/2 pairs per block)
+            uint32_t bb, i;
+            fast_divmod(j, a.nest_rows, a.inv_nest_rows, bb, i);
+            cx = (2 * bb + a.nest_s) * a.nest_B + 2 * i + a.colour;
+        } else {
+            cx = 2 * j + a.colour;
+        }
     } else {
-        cy = 2 * rowsel + (a.colour >> 1);
-        cx = 2 * j + (a.colour & 1);
+        uint32_t y0 = 0;          // first local row of the active outer block (f3), else 0
+        if (NEST) {
+            uint32_t bb, i;
+            fast_divmod(rowsel, a.nest_rows, a.inv_nest_rows, bb, i);
+            y0 = (2 * bb + a.nest_s) * a.nest_B;
+            rowsel = i;
+        }
+        if (a.C == 2) {
+            cy = y0 + rowsel;
+            cx = 2 * j + ((a.colour + g.row_offset + cy) & 1);
+        } else {
+            cy = y0 + 2 * rowsel + (a.colour >> 1);
+            cx = 2 * j + (a.colour & 1);
+        }
     }
     const uint32_t gy = g.row_offset + cy;
     const uint32_t rowlen = (uint32_t)g.R * g.Mx;
@@ -86,7 +100,7 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     return L;
 }
 
-template <int KIND, int NDIM, int BS, int MINB, bool MH>
+template <int KIND, int NDIM, int BS, int MINB, bool MH, bool NEST>
 __global__ void __launch_bounds__(BS, MINB)
 substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
     using M = Model<KIND, NDIM>;
@@ -120,7 +134,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
 
     // a3: stage the closure (cell + one-site halo) of cell `ci` into registers
     auto load = [&](uint32_t c) {
-        const CellLoc L = locate<NDIM>(a, c);
+        const CellLoc L = locate<NDIM, NEST>(a, c);
         gid32 = L.gid32;
         iCcur = L.iC;
         k = 0;
@@ -141,7 +155,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
             evsum += k;
             return;
         }
-        const CellLoc L = locate<NDIM>(a, c);
+        const CellLoc L = locate<NDIM, NEST>(a, c);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             uint64_t* pl = planes[p];
@@ -216,28 +230,12 @@ static int resident_ctas(K kernel, int bs) {
     return per * nsm;
 }
 
-template <int KIND, int NDIM>
-static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
-    if (nactive <= 0) return cudaSuccess;
-    // launch shape experiments: KMC_LB=3 forces the 128-register build, KMC_LB=4 the 80-register one
-    static const int lb = [] { const char* e = getenv("KMC_LB"); return e ? atoi(e) : 0; }();
-    static const int mh_env = [] { const char* e = getenv("KMC_MH"); return e ? atoi(e) : -1; }();
+template <int KIND, int NDIM, int MINB, bool MH, bool NEST>
+static cudaError_t launch_v(const SubstepArgs& a, long long nactive, cudaStream_t s) {
     constexpr int bs = 256;
-    // merged halo boards need disjoint first/last columns (and rows in 2D).  Spin flip: the four
-    // separate (window-constant) boards save 8 logic ops per event and measured 3 % faster at
-    // dt = 1, so merged boards are opt-in there (KMC_MH=1).
-    const bool mh = a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2) && !(KIND == 0 && mh_env != 1);
-    // hop / pair models: diffusion (22 masks live) is fastest with <= 128 registers (2 CTAs/SM),
-    // ZGB (counts + rebuilt mask) with <= 80 registers (3 CTAs/SM) -- measured on B200
-    const bool big = KIND != 0 && ((KIND == 1 && lb != 4) || lb == 3);
-    // spin flip: <= 64 registers (61 used, no spills) -> 4 CTAs of 256 per SM; KMC_LB=6: <= 80
-    const bool four = KIND == 0 && !mh && lb != 6;
-    auto kern = KIND == 0 ? (mh ? substep_kernel<KIND, NDIM, bs, 3, true>
-                                : (four ? substep_kernel<KIND, NDIM, bs, 4, false> : substep_kernel<KIND, NDIM, bs, 3, false>))
-                          : (big ? substep_kernel<KIND, NDIM, bs, 2, true> : substep_kernel<KIND, NDIM, bs, 3, true>);
-    // persistent grid: one wave of resident warps, each starting on its own chunk of 32*cpl cells
-    static int cap_q3 = 0, cap_q2 = 0, cap_nm = 0, cap_4 = 0;
-    int& cap = KIND == 0 ? (mh ? cap_q3 : (four ? cap_4 : cap_nm)) : (big ? cap_q2 : cap_q3);
+    auto kern = substep_kernel<KIND, NDIM, bs, MINB, MH, NEST>;
+    // persistent grid: one wave of resident warps, each starting on its own chunk of 32*8 cells
+    static int cap = 0;                                            // per instantiation
     if (cap == 0) cap = resident_ctas(kern, bs);
     const long long chunk = 32 * 8;
     const long long want = (nactive + chunk - 1) / chunk;          // warps if every warp took one chunk
@@ -247,6 +245,35 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
     if (e != cudaSuccess) return e;
     kern<<<nb, bs, 0, s>>>(a, (uint32_t)nactive, (uint32_t)chunk);
     return cudaGetLastError();
+}
+
+template <int KIND, int NDIM>
+static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
+    if (nactive <= 0) return cudaSuccess;
+    // launch shape experiments: KMC_LB=3 forces the 128-register build, KMC_LB=4 the 80-register one,
+    // KMC_LB=6 the 80-register spin-flip build; KMC_MH=1 merged halo boards for spin flip
+    static const int lb = [] { const char* e = getenv("KMC_LB"); return e ? atoi(e) : 0; }();
+    static const int mh_env = [] { const char* e = getenv("KMC_MH"); return e ? atoi(e) : -1; }();
+    // merged halo boards need disjoint first/last columns (and rows in 2D)
+    const bool mh_ok = a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2);
+    if constexpr (KIND == 0) {
+        // spin flip: the four separate (window-constant) halo boards save 8 logic ops per event and
+        // measured 3 % faster at dt = 1; <= 64 registers (no spills) -> 4 CTAs of 256 per SM
+        if (a.nest) return launch_v<KIND, NDIM, 4, false, true>(a, nactive, s);
+        if (mh_ok && mh_env == 1) return launch_v<KIND, NDIM, 3, true, false>(a, nactive, s);
+        if (lb == 6) return launch_v<KIND, NDIM, 3, false, false>(a, nactive, s);
+        return launch_v<KIND, NDIM, 4, false, false>(a, nactive, s);
+    } else {
+        // hop / pair models need the merged boards (qx, qy >= 2 is enforced at create).  Diffusion
+        // (22 masks live) is fastest with <= 128 registers (2 CTAs/SM), ZGB (counts + rebuilt mask)
+        // with <= 80 registers (3 CTAs/SM) -- measured on B200
+        if (!mh_ok) return cudaErrorInvalidValue;
+        const bool big = (KIND == 1 && lb != 4) || lb == 3;
+        if (a.nest) return big ? launch_v<KIND, NDIM, 2, true, true>(a, nactive, s)
+                               : launch_v<KIND, NDIM, 3, true, true>(a, nactive, s);
+        return big ? launch_v<KIND, NDIM, 2, true, false>(a, nactive, s)
+                   : launch_v<KIND, NDIM, 3, true, false>(a, nactive, s);
+    }
 }
 
 cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cudaStream_t s) {

@@ -314,3 +314,71 @@ def test_multiscale_bit_exact(ndim, dims, cell, kind, params, inner, nf):
         orc.run_multiscale(1.0, 0.5, nf, inner)
         assert_same_state(gpu, orc, f"multiscale {kind} {inner}")
     assert orc.events > 0
+
+
+NESTED = [
+    # ndim, dims, cell, kind, params, block, outer, inner, n_inner
+    (2, (64, 128), (8, 8), "adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), 2, "lie", "lie", 2),
+    (2, (64, 64), (4, 4), "zgb", dict(k1=0.45, k2=1.0), 4, "strang", "strang", 2),
+    (2, (32, 64), (4, 4), "adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), 2, "lie", "random", 3),
+    (1, (1024,), (32,), "adsdes", dict(ca=1, cd=1, beta=2.0, K=1.0, h=-0.5), 4, "strang", "lie", 1),
+    (1, (256,), (4,), "zgb_diff", dict(k1=0.4, k2=1.0, c_hop=0.8), 8, "lie", "strang", 2),
+]
+
+
+@pytest.mark.parametrize("ndim,dims,cell,kind,params,block,outer,inner,n_inner", NESTED)
+def test_nested_bit_exact(ndim, dims, cell, kind, params, block, outer, inner, n_inner):
+    """f3: kmc_run_nested (eq.(opdecomp2), R28) is bit-exact vs O2's run_nested after every call."""
+    gpu, orc = make_pair(ndim, dims, cell, kind, params, 0, 2)
+    lat = (si.bernoulli_lattice(gpu.local_shape, 0.4, seed=14) if kind.startswith("adsdes")
+           else si.categorical_lattice(gpu.local_shape, [0.5, 0.3, 0.2], seed=14))
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    for i in range(2):
+        t1 = gpu.run_nested(1.0, 0.5, n_inner, outer, inner, block)
+        t2 = orc.run_nested(1.0, 0.5, n_inner, outer, inner, block)
+        assert t1 == t2 is False
+        assert_same_state(gpu, orc, f"nested {kind} {outer}/{inner} call {i}")
+    assert orc.events > 0
+
+
+@pytest.mark.parametrize("kind,params,cell,block", [
+    ("adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), (8, 8), 2),
+    ("adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), (4, 4), 2),
+    ("zgb", dict(k1=0.45, k2=1.0), (4, 4), 4),
+])
+@pytest.mark.parametrize("world", [2, 4])
+def test_nested_virtual_ranks_bit_identical(kind, params, cell, block, world):
+    """f3 on G virtual ranks: ONE halo exchange (+ reverse XOR deltas) per outer factor instead of
+    per window gives the bit-identical result of G = 1 -- the ghost rows belong to the inactive
+    outer colour for the whole factor (R28)."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    dims = (64, 32) if cell == (8, 8) else (64, 16)
+    one = kmc.KMC(2, dims, cell, kind=kind, seed=35, replicas=2, **params)
+    grp = kmc.VGroup(world, dims, cell, kind=kind, seed=35, replicas=2, **params)
+    if (dims[0] // cell[0]) // world % block:
+        pytest.skip("blocks would straddle ranks")
+    lat = (si.bernoulli_lattice(one.local_shape, 0.5, seed=3) if kind != "zgb"
+           else si.categorical_lattice(one.local_shape, [0.5, 0.25, 0.25], seed=3))
+    one.set_config(lat)
+    grp.set_config(lat)
+    for outer, inner, n in (("lie", "lie", 3), ("strang", "strang", 2)):
+        one.run_nested(1.0, 0.5, n, outer, inner, block)
+        grp.run_nested(1.0, 0.5, n, outer, inner, block)
+        assert np.array_equal(one.get_config(), grp.get_config()), (outer, inner)
+    a, b = one.observables(), grp.observables()
+    assert a["events"] == b["events"] > 0
+
+
+def test_nested_errors():
+    """kmc_run_nested argument checks (include/kmc.h): KMC_EINVAL / KMC_EPARTITION."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    g = kmc.KMC(2, (48, 64), (8, 8), kind="adsdes", seed=1)     # 6 cell rows
+    for args, code in [((1, "lie", "lie", 3), 1), ((0, "lie", "lie", 2), 1), ((1, "random", "lie", 2), 1),
+                       ((1, "lie", "lie", 2), 2), ((1, "lie", "lie", 6), 2)]:
+        with pytest.raises(kmc.KmcError) as e:
+            g.run_nested(1.0, 0.5, *args)
+        assert e.value.status == code, (args, e.value)
+    assert g.observables()["windows"] == 0          # nothing ran
