@@ -48,6 +48,7 @@ struct SubstepArgs {
     // cell rows in 2D, cells in 1D) of one outer colour.  nest = 0: off.  In 2D the active rows are
     // numbered block by block, nest_rows per block; nest_s = parity of the first local block
     // that is active.
+    int refill_min;                  // parked finished lanes that trigger a warp's refill (>= 1)
     int nest, nest_B, nest_s;
     uint32_t nest_rows;
     double inv_nest_rows;

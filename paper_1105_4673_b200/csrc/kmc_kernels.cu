@@ -109,7 +109,9 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     const unsigned FULL = 0xffffffffu;
     // log_spec tables -> shared memory (lanes index them by their own bucket)
     __shared__ double s_logc[kLogTab], s_logl[kLogTab];
+    __shared__ uint8_t s_sel8[kSel8];
     for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) { s_logc[i] = a.log_c[i]; s_logl[i] = a.log_l[i]; }
+    init_sel8(s_sel8);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -186,10 +188,19 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     // The event step is one branch-free basic block: lanes without a cell (queue exhausted) and
     // lanes whose window ended compute it too, with the update masked off, so the warp never
     // diverges inside the step and the scheduler can interleave its independent chains.
+    // A lane whose window ends parks its finished cell (pend) until at least refill_min lanes are
+    // parked (or none is running): the write-back + refill block costs the whole warp about half an
+    // event step, so batching it trades a little lane idling for fewer executions.
+    bool pend = false;
+    const uint32_t refill_min = (uint32_t)a.refill_min;
     for (;;) {
-        const bool fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logc, s_logl);
-        const unsigned fm = __ballot_sync(FULL, fin);
-        if (fm) {                                                  // warp-uniform
+        const bool fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logc, s_logl, s_sel8);
+        pend = pend || fin;
+        have = have && !fin;
+        const unsigned fm = __ballot_sync(FULL, pend);
+        if (fm && (__popc(fm) >= refill_min || !__any_sync(FULL, have))) {   // warp-uniform
+            const bool fin = pend;
+            pend = false;
             const uint32_t need = __popc(fm);
             const uint32_t rank = __popc(fm & ((1u << lane) - 1u));
             const uint32_t avail = cend > next ? cend - next : 0u;
