@@ -108,9 +108,9 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     const Geo& g = a.g;
     const unsigned FULL = 0xffffffffu;
     // log_spec tables -> shared memory (lanes index them by their own bucket)
-    __shared__ double s_logc[kLogTab], s_logl[kLogTab];
+    __shared__ double2 s_logt[kLogTab];
     __shared__ uint8_t s_sel8[kSel8];
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) { s_logc[i] = a.log_c[i]; s_logl[i] = a.log_l[i]; }
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = make_double2(a.log_c[i], a.log_l[i]);
     init_sel8(s_sel8);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -194,7 +194,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     bool pend = false;
     const uint32_t refill_min = (uint32_t)a.refill_min;
     for (;;) {
-        const bool fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logc, s_logl, s_sel8);
+        const bool fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
         pend = pend || fin;
         have = have && !fin;
         const unsigned fm = __ballot_sync(FULL, pend);

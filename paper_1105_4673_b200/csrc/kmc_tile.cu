@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256, 3)
 tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
     constexpr int SW = TX + 2;                       // smem row stride (words)
     __shared__ uint64_t T[(TY + 2) * SW];
-    __shared__ double s_logc[kLogTab], s_logl[kLogTab];
+    __shared__ double2 s_logt[kLogTab];
     __shared__ uint8_t s_sel8[kSel8];
     __shared__ uint32_t s_next;
     const Geo& g = a.g;
@@ -38,7 +38,7 @@ tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
     const uint32_t rowlen = (uint32_t)g.R * g.Mx;
     const uint32_t rbase = (uint32_t)r * g.Mx;
 
-    for (int i = tid; i < kLogTab; i += blockDim.x) { s_logc[i] = a.log_c[i]; s_logl[i] = a.log_l[i]; }
+    for (int i = tid; i < kLogTab; i += blockDim.x) s_logt[i] = make_double2(a.log_c[i], a.log_l[i]);
     init_sel8(s_sel8);
     if (tid == 0) s_next = blockDim.x;
     // a3: the tile and its halo ring, row by row (coalesced), periodic wrap / ghost rows
@@ -85,7 +85,7 @@ tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
     if (have) load();
     if (!__any_sync(FULL, have)) return;                          // warp beyond the tile's cells
     for (;;) {
-        const bool fin = event_step<0, 2, MH>(a, P, hb, k, tclock, gid32, have, s_logc, s_logl, s_sel8);
+        const bool fin = event_step<0, 2, MH>(a, P, hb, k, tclock, gid32, have, s_logt, s_sel8);
         const unsigned fm = __ballot_sync(FULL, fin);
         if (fm) {                                                   // warp-uniform
             uint32_t base = 0;
