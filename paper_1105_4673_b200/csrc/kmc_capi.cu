@@ -120,7 +120,7 @@ struct kmc_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
-    double tile_rate_bound = 0.0;            // rough events per unit time per cell (kernel choice)
+    double rate_per_cell = 0.0;            // rough events per unit time per cell (kernel choice)
     int kernel_mode = 0;                     // kmc_set_kernel
     SubstepArgs args{};                      // window-invariant kernel arguments (build_args_template)
     struct VgShared* vg_shared = nullptr;    // virtual-rank group stream (reference counted)
@@ -295,11 +295,7 @@ void build_args_template(kmc_ctx* c) {
     a.queue = c->queue;
     a.C = c->C;
     a.inv_scale = std::ldexp(1.0, -c->F);
-    // refill batching of the window kernel (performance only; results are bit-identical)
-    static const int refill_env = [] { const char* e = getenv("KMC_REFILL"); return e ? atoi(e) : 0; }();
-    // measured on B200 (tools/sweep_refill.sh): spin flip 3 (+3 %), diffusion 4 (+10 %), ZGB 8 (+6 %)
-    static const int refill_default[4] = {3, 4, 8, 8};
-    a.refill_min = refill_env >= 1 && refill_env <= 32 ? refill_env : refill_default[c->kind & 3];
+    a.refill_min = 1;                       // set per window (launch_window)
     a.half = (uint32_t)(c->g.Mx / 2);
     a.inv_half = 1.0 / (double)a.half;
     a.inv_R = 1.0 / (double)c->g.R;
@@ -357,6 +353,15 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     a.colour = colour;
     a.D = D;
     const long long nactive = nest ? apply_nest(c, *nest, a) : active_cells(c);
+    // refill batching of the window kernel (performance only; results are bit-identical): a warp
+    // refills its finished lanes once refill_min of them are parked.  Best thresholds measured on
+    // B200 (tools/sweep_refill.sh) depend on the expected events per cell-window mu ~ D x
+    // rate_per_cell: mu >= 16 (Ising dt = 1, diffusion): spin flip 3, diffusion 4; mu < 16
+    // (Ising dt = 0.01, ZGB dt = 0.1): spin flip 10, ZGB 16 (+8 % over 8).  Env KMC_REFILL overrides.
+    static const int refill_env = [] { const char* e = getenv("KMC_REFILL"); return e ? atoi(e) : 0; }();
+    static const int refill_hi[4] = {3, 4, 6, 6}, refill_lo[4] = {10, 10, 16, 16};
+    a.refill_min = refill_env >= 1 && refill_env <= 32 ? refill_env
+                 : (D * c->rate_per_cell >= 16.0 ? refill_hi[c->kind & 3] : refill_lo[c->kind & 3]);
     a.w_lo = (uint32_t)c->window;
     a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
     if (class_mask != ~0ull)
@@ -638,7 +643,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     {   // kernel-choice heuristic: sites x mean class rate ~ events per unit time per cell
         double s = 0.0;
         for (int i = 0; i < c->nclass; ++i) s += c->crate[i];
-        c->tile_rate_bound = (double)g.nsite * s / (double)c->nclass;
+        c->rate_per_cell = (double)g.nsite * s / (double)c->nclass;
     }
 
     cudaError_t e = cudaSetDevice(c->device);
