@@ -122,6 +122,15 @@ kmc_status kmc_get_config(kmc_ctx* ctx, uint8_t* host_local_slab, int64_t nbytes
  * (out-of-range spins are clamped to vacant and counted; see kmc_observables). */
 kmc_status kmc_set_config_device(kmc_ctx* ctx, const uint8_t* dev_local_slab, int64_t nbytes);
 kmc_status kmc_get_config_device(kmc_ctx* ctx, uint8_t* dev_local_slab, int64_t nbytes);
+/* Bit-packed local slab (host buffers; the checkpoint format and the cheap upload path -- 1 bit per
+ * site and plane instead of 1 byte per site): nwords = planes x rows_local/q_y x replicas_local x
+ * W/q_x u64 words in the library's own layout [plane][cell row][replica][cell column] (DESIGN.md
+ * §7): bit (ly*q_x + lx) of a word = site (cy*q_y + ly, cx*q_x + lx) of that replica.  Plane 0 =
+ * occupied (ads/des models) or CO (ZGB); plane 1 = O (ZGB only).  set validates: bits beyond the
+ * q_x*q_y sites of a cell, or a site both CO and O, give KMC_EINVAL and leave the lattice unchanged.
+ * Synchronous. */
+kmc_status kmc_set_config_packed(kmc_ctx* ctx, const uint64_t* host_words, int64_t nwords);
+kmc_status kmc_get_config_packed(kmc_ctx* ctx, uint64_t* host_words, int64_t nwords);
 
 /* Advance physical time by T with macro-steps of dt (R20: n = ceil(T/dt - 1e-9) macro-steps, the
  * last of duration T - (n-1) dt; KMC_WTRUNCATED if it differs from dt).  Lie: colours 0..C-1 for

@@ -28,7 +28,7 @@ EXPORTS = [
     "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
     "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
     "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale", "kmc_run_nested",
-    "kmc_vgroup_run_nested",
+    "kmc_vgroup_run_nested", "kmc_set_config_packed", "kmc_get_config_packed",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -104,6 +104,8 @@ def lib():
         "kmc_run_multiscale": ([vp, dbl, dbl, i32, i32, u64], i32),
         "kmc_run_nested": ([vp, dbl, dbl, i32, i32, i32, i32], i32),
         "kmc_vgroup_run_nested": ([vp, i32, dbl, dbl, i32, i32, i32, i32], i32),
+        "kmc_set_config_packed": ([vp, vp, i64], i32),
+        "kmc_get_config_packed": ([vp, vp, i64], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -181,6 +183,9 @@ class KMC:
         self.local_shape = (rl.value, hl.value, w.value)
         self.replica_offset, self.row_offset = ro.value, yo.value
         self.nbytes = rl.value * hl.value * w.value
+        qy, qx = (1, int(cell[0])) if int(ndim) == 1 else (int(cell[0]), int(cell[1]))
+        # bit-packed layout [plane][cell row][replica][cell column] (kmc_set_config_packed)
+        self.packed_shape = (2 if self.nstates == 3 else 1, hl.value // qy, rl.value, w.value // qx)
 
     def _check(self, st, allow=()):
         if st != KMC_OK and st not in allow:
@@ -209,6 +214,18 @@ class KMC:
     def get_config(self):
         out = np.empty(self.local_shape, dtype=np.uint8)
         self._check(self._L.kmc_get_config(self._ctx, out.ctypes.data, out.size))
+        return out
+
+    def set_config_packed(self, words):
+        """Host uint64 words in packed_shape (kmc_set_config_packed: 1 bit per site and plane)."""
+        a = np.ascontiguousarray(words, dtype=np.uint64)
+        if a.size != int(np.prod(self.packed_shape)):
+            raise ValueError(f"expected {int(np.prod(self.packed_shape))} words, got {a.size}")
+        self._check(self._L.kmc_set_config_packed(self._ctx, a.ctypes.data, a.size))
+
+    def get_config_packed(self):
+        out = np.empty(self.packed_shape, dtype=np.uint64)
+        self._check(self._L.kmc_get_config_packed(self._ctx, out.ctypes.data, out.size))
         return out
 
     def set_config_device(self, ptr, nbytes):

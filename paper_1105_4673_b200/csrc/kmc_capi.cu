@@ -787,6 +787,46 @@ kmc_status kmc_get_config(kmc_ctx* c, uint8_t* host, int64_t nbytes) {
     return KMC_OK;
 }
 
+// Bit-packed slab: [plane][owned cell row][replica][cx] u64 words, exactly the owned rows of the
+// device planes, so H2D / D2H are one contiguous copy per plane (8x fewer bytes than uint8 sites).
+static long long packed_words(const kmc_ctx* c) { return (long long)c->nplanes * c->g.My_local * c->g.R * c->g.Mx; }
+
+kmc_status kmc_set_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nwords) {
+    if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nwords != packed_words(c)) return fail(c, KMC_EINVAL, "nwords %lld != packed local slab %lld", (long long)nwords, packed_words(c));
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    for (int p = 0; p < c->nplanes; ++p)
+        if (!c->spare[p] && cudaMalloc((void**)&c->spare[p], (size_t)c->plane_words * 8) != cudaSuccess)
+            return fail(c, KMC_ENOMEM, "spare plane allocation failed");
+    const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
+    const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
+    CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));
+    for (int p = 0; p < c->nplanes; ++p) {
+        if (c->g.ghost)   // ghost rows are refreshed by the next exchange; keep them defined
+            CUDA_TRY(c, cudaMemcpyAsync(c->spare[p], c->planes[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_TRY(c, cudaMemcpyAsync(c->spare[p] + off, host + (size_t)p * owned, owned * 8, cudaMemcpyHostToDevice, c->stream));
+    }
+    CUDA_TRY(c, launch_check_packed(c->spare[0] + off, c->nplanes > 1 ? c->spare[1] + off : nullptr, (long long)owned,
+                                    c->g.valid, c->err_flag, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->err_flag, 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (*c->h_err) return fail(c, KMC_EINVAL, "packed configuration has bits outside the cells or a site both CO and O");
+    for (int p = 0; p < c->nplanes; ++p) std::swap(c->spare[p], c->planes[p]);
+    return KMC_OK;
+}
+
+kmc_status kmc_get_config_packed(kmc_ctx* c, uint64_t* host, int64_t nwords) {
+    if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nwords != packed_words(c)) return fail(c, KMC_EINVAL, "nwords %lld != packed local slab %lld", (long long)nwords, packed_words(c));
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
+    const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
+    for (int p = 0; p < c->nplanes; ++p)
+        CUDA_TRY(c, cudaMemcpyAsync(host + (size_t)p * owned, c->planes[p] + off, owned * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return KMC_OK;
+}
+
 kmc_status kmc_substep(kmc_ctx* c, int32_t colour, double duration) {
     if (!c) return KMC_EINVAL;
     if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: use kmc_vgroup_run");

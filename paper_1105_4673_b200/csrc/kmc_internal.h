@@ -89,6 +89,8 @@ cudaError_t launch_pack(const Geo& g, const uint8_t* in, uint64_t* p0, uint64_t*
                         unsigned int* err, cudaStream_t s);
 cudaError_t launch_unpack(const Geo& g, const uint64_t* p0, const uint64_t* p1, int nplanes,
                           uint8_t* out, cudaStream_t s);
+cudaError_t launch_check_packed(const uint64_t* p0, const uint64_t* p1, long long n, uint64_t valid,
+                                unsigned int* err, cudaStream_t s);
 cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* a, const uint64_t* b, long long n, cudaStream_t s);
 
 }  // namespace kmc

@@ -558,6 +558,28 @@ cudaError_t launch_unpack(const Geo& g, const uint64_t* p0, const uint64_t* p1, 
     return cudaGetLastError();
 }
 
+// validation of a bit-packed slab (kmc_set_config_packed): no bits outside the cell's sites, and in
+// the two-plane models no site both CO and O
+__global__ void check_packed_kernel(const uint64_t* __restrict__ p0, const uint64_t* __restrict__ p1,
+                                    long long n, uint64_t valid, unsigned int* err) {
+    unsigned bad = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const uint64_t a = p0[i];
+        const uint64_t b = p1 ? p1[i] : 0ull;
+        bad |= ((a | b) & ~valid) != 0 || (a & b) != 0;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+cudaError_t launch_check_packed(const uint64_t* p0, const uint64_t* p1, long long n, uint64_t valid,
+                                unsigned int* err, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    long long nb = (n + 255) / 256;
+    if (nb > 148 * 16) nb = 148 * 16;
+    check_packed_kernel<<<(unsigned)nb, 256, 0, s>>>(p0, p1, n, valid, err);
+    return cudaGetLastError();
+}
+
 __global__ void xor_into_kernel(uint64_t* dst, const uint64_t* src, long long n) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] ^= src[i];

@@ -50,6 +50,23 @@ def colour_full_lattice(shape, ndim, cell, C, colour=1):
     return np.broadcast_to((col == colour).astype(np.uint8), shape).copy()
 
 
+def packed_lattice(lat, ndim, cell, nplanes):
+    """The same input in the library's bit-packed upload format (kmc_set_config_packed, layout
+    [plane][cell row][replica][cell column], bit ly*q_x + lx of a word = site (ly, lx) of the cell,
+    plane p = (site == p + 1)).  Layout conversion only; q_x must be a multiple of 8."""
+    R, H, W = lat.shape
+    qy, qx = (1, cell[0]) if ndim == 1 else cell
+    if qx % 8 or qx * qy > 64:
+        raise ValueError("packed_lattice needs q_x % 8 == 0 and q_x*q_y <= 64")
+    My, Mx, nb = H // qy, W // qx, qx * qy // 8
+    out = np.zeros((nplanes, My, R, Mx, 8), dtype=np.uint8)
+    for p in range(nplanes):
+        b = np.packbits(lat == p + 1, axis=2, bitorder="little")          # [R][H][W/8]
+        b = b.reshape(R, My, qy, Mx, qx // 8).transpose(1, 0, 3, 2, 4).reshape(My, R, Mx, nb)
+        out[p, ..., :nb] = b
+    return out.view(np.uint64).reshape(nplanes, My, R, Mx)
+
+
 # Named workloads (DESIGN.md §6; SURVEY §8(d) table).
 WORKLOADS = {
     # target / bench N=1: 2D Ising ads/des 32768^2, 8x8 cells, Lie dt=1,

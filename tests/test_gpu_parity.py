@@ -382,3 +382,69 @@ def test_nested_errors():
             g.run_nested(1.0, 0.5, *args)
         assert e.value.status == code, (args, e.value)
     assert g.observables()["windows"] == 0          # nothing ran
+
+
+def _pack_words(lat, qy, qx, nplanes):
+    """The documented kmc_set_config_packed layout, written out with numpy (test helper):
+    words[p][cy][r][cx] bit (ly*qx + lx) = (site value == p + 1)."""
+    R, H, W = lat.shape
+    My, Mx = H // qy, W // qx
+    out = np.zeros((nplanes, My, R, Mx), dtype=np.uint64)
+    weights = (np.uint64(1) << np.arange(qy * qx, dtype=np.uint64))
+    for p in range(nplanes):
+        b = (lat == p + 1).reshape(R, My, qy, Mx, qx).transpose(1, 0, 3, 2, 4).reshape(My, R, Mx, qy * qx)
+        out[p] = (b.astype(np.uint64) * weights).sum(axis=-1, dtype=np.uint64)
+    return out
+
+
+@pytest.mark.parametrize("ndim,dims,cell,kind,R", [
+    (2, (64, 96), (8, 8), "adsdes", 2),
+    (2, (32, 48), (4, 2), "zgb", 3),
+    (1, (512,), (32,), "adsdes", 4),
+    (1, (96,), (6,), "zgb_diff", 2),
+])
+def test_packed_config_roundtrip_and_run(ndim, dims, cell, kind, R):
+    """kmc_set/get_config_packed: the documented bit layout (numpy packing) round-trips against the
+    uint8 path, and a run from a packed upload is bit-identical to a run from the uint8 upload."""
+    gpu, orc = make_pair(ndim, dims, cell, kind, {}, 0, R)
+    lat = (si.bernoulli_lattice(gpu.local_shape, 0.45, seed=21) if kind == "adsdes"
+           else si.categorical_lattice(gpu.local_shape, [0.4, 0.35, 0.25], seed=21))
+    qy, qx = (1, cell[0]) if ndim == 1 else cell
+    words = _pack_words(lat, qy, qx, gpu.packed_shape[0])
+    assert words.shape == gpu.packed_shape
+    gpu.set_config(lat)
+    assert np.array_equal(gpu.get_config_packed(), words)
+    import paper_1105_4673_b200 as kmc
+    g2 = kmc.KMC(ndim, dims, cell, kind=kind, replicas=R, seed=1234)
+    g2.set_config_packed(words)
+    assert np.array_equal(g2.get_config(), lat)
+    gpu.run(1.0, 0.5, "strang")
+    g2.run(1.0, 0.5, "strang")
+    assert np.array_equal(gpu.get_config(), g2.get_config())
+    orc.set_config(lat)
+    orc.run(1.0, 0.5, "strang")
+    assert np.array_equal(g2.get_config(), orc.get_config())
+
+
+def test_packed_config_validation():
+    """Bits outside a cell's sites (cell of 8 sites) and CO+O on one site are KMC_EINVAL; the
+    lattice is left unchanged."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    g = kmc.KMC(2, (16, 16), (4, 2), kind="zgb", seed=3)
+    lat = si.categorical_lattice(g.local_shape, [0.5, 0.25, 0.25], seed=4)
+    g.set_config(lat)
+    w = g.get_config_packed()
+    bad = w.copy()
+    bad[0, 0, 0, 0] |= np.uint64(1) << np.uint64(8)              # site 8 of a 4x2 cell does not exist
+    with pytest.raises(kmc.KmcError) as e:
+        g.set_config_packed(bad)
+    assert e.value.status == 1
+    bad = w.copy()
+    bad[1, 1, 0, 1] |= bad[0, 1, 0, 1] | np.uint64(1)             # a site both CO and O
+    bad[0, 1, 0, 1] |= np.uint64(1)
+    with pytest.raises(kmc.KmcError):
+        g.set_config_packed(bad)
+    assert np.array_equal(g.get_config(), lat)
+    with pytest.raises(ValueError):
+        g.set_config_packed(w[:, :1])

@@ -46,14 +46,19 @@ for a, t, _ in rows:
         tgt = labels[m.group(1)]
         if tgt < a and (best is None or a - tgt > best[1] - best[0]):
             best = (tgt, a)
+region = sys.argv[3] if len(sys.argv) > 3 else "step"     # "step" or "refill" (rest of the loop)
 step = []
+seen_vote = False
 for a, t, ln in rows:
-    if a < best[0]:
+    if a < best[0] or a > best[1]:
         continue
-    step.append((t, ln))
+    if region == "step" or seen_vote:
+        step.append((t, ln))
     if "VOTE" in t:
-        break
-print(len(step), "instructions in the event step")
+        if region == "step":
+            break
+        seen_vote = True
+print(len(step), "instructions in the", region, "region")
 cnt = collections.Counter(ln for _, ln in step)
 src = {}
 for (f, n), c in sorted(cnt.items(), key=lambda x: -x[1]):
