@@ -248,9 +248,13 @@ static cudaError_t launch_v(const SubstepArgs& a, long long nactive, cudaStream_
     // persistent grid: one wave of resident warps, each starting on its own chunk of 32*8 cells
     static int cap = 0;                                            // per instantiation
     if (cap == 0) cap = resident_ctas(kern, bs);
-    const long long chunk = 32 * 8;
+    // chunk = 256 cells per claim; smaller windows get smaller chunks (multiples of 32, one cell per
+    // lane at least) so that the grid still fills every resident warp slot
+    const long long cap_warps = (long long)cap * (bs / 32);
+    long long chunk = 32 * 8;
+    while (chunk > 32 && (nactive + chunk - 1) / chunk < cap_warps) chunk -= 32;
     const long long want = (nactive + chunk - 1) / chunk;          // warps if every warp took one chunk
-    const long long nwarps = want < (long long)cap * (bs / 32) ? want : (long long)cap * (bs / 32);
+    const long long nwarps = want < cap_warps ? want : cap_warps;
     const unsigned nb = (unsigned)((nwarps * 32 + bs - 1) / bs);
     cudaError_t e = cudaMemsetAsync(a.queue, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
