@@ -85,6 +85,10 @@ typedef struct {
     int32_t device;               /* CUDA device ordinal */
     const uint8_t* nccl_unique_id;/* 128 bytes from kmc_nccl_unique_id() on rank 0, broadcast; NULL if world = 1 */
     void* stream;                 /* cudaStream_t to launch on (e.g. torch's current stream); NULL = library-owned */
+    const int64_t* row_bounds;    /* 2D, world > 1: world+1 cell-row bounds of the slabs (rank r owns cell rows
+                                     [b_r, b_{r+1}), each an even number >= 2; e.g. from
+                                     kmc_workload_partition), NULL = the even split.  Results do not depend
+                                     on the split (global ids).  KMC_EPARTITION if invalid. */
 } kmc_dist;
 
 typedef struct {
@@ -224,6 +228,30 @@ kmc_status kmc_vgroup_sync(kmc_ctx** ctxs, int32_t world);
 /* kmc_run_nested on a virtual-rank group (one exchange per outer factor). */
 kmc_status kmc_vgroup_run_nested(kmc_ctx** ctxs, int32_t world, double T, double dt, int32_t n_inner,
                                  kmc_scheme outer, kmc_scheme inner, int32_t block);
+
+/* kmc_vgroup_create with caller-chosen slabs (row_bounds as in kmc_dist; NULL = even split). */
+kmc_status kmc_vgroup_create_bounds(const kmc_geometry* geom, const kmc_model* model, int32_t world, int32_t device,
+                                    void* stream, const int64_t* row_bounds, kmc_ctx** out);
+
+/* Workload re-balancing ("Mass Transport and Dynamic Workload Balancing",
+ * P:885-940; R29).  The workload of eq.(wload) is the per-cell event count
+ * since the last kmc_workload_mark (or since kmc_create).  It is summed over strips -- cell rows in
+ * 2D (all columns and replicas), cells in 1D (all replicas) -- and the cdf of the strip
+ * loads is mapped onto `parts` groups of equal mass: raw bound b_l = min{s+1 :
+ * parts * cdf(s) >= l * S}, rounded to the nearest multiple of `granule` strips (ties up) and
+ * clamped so that every group keeps >= granule strips; no events gives the even split.
+ * bounds (host, parts+1 entries) receives b_0 = 0 < ... < b_parts = strips; in 2D with granule 2
+ * they are valid kmc_dist.row_bounds for `parts` ranks.  strip_load (host, nullable, one u64 per
+ * strip) receives the loads; imbalance (host, nullable, 2 doubles) = max group load x parts / S for
+ * the cdf bounds and for the even split.  world > 1: the strip loads are summed over ranks (NCCL),
+ * every rank gets the same bounds.  KMC_EINVAL: parts outside [1, 4096], strips not a multiple of
+ * granule or fewer than parts*granule.  Requires parts * S < 2^64.  Synchronous. */
+kmc_status kmc_workload_mark(kmc_ctx* ctx);
+kmc_status kmc_workload_partition(kmc_ctx* ctx, int32_t parts, int32_t granule, int64_t* bounds, uint64_t* strip_load,
+                                  double* imbalance);
+/* The same over a virtual-rank group (strip loads of all ranks). */
+kmc_status kmc_vgroup_workload_partition(kmc_ctx** ctxs, int32_t world, int32_t parts, int32_t granule, int64_t* bounds,
+                                         uint64_t* strip_load, double* imbalance);
 
 /* NCCL unique id for world > 1 (rank 0 calls it and broadcasts the 128 bytes). */
 kmc_status kmc_nccl_unique_id(uint8_t out[128]);

@@ -29,6 +29,7 @@ EXPORTS = [
     "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
     "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale", "kmc_run_nested",
     "kmc_vgroup_run_nested", "kmc_set_config_packed", "kmc_get_config_packed",
+    "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -46,7 +47,7 @@ class KmcGeometry(ctypes.Structure):
 
 class KmcDist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("row_bounds", ctypes.c_void_p)]
 
 
 class KmcObs(ctypes.Structure):
@@ -106,6 +107,10 @@ def lib():
         "kmc_vgroup_run_nested": ([vp, i32, dbl, dbl, i32, i32, i32, i32], i32),
         "kmc_set_config_packed": ([vp, vp, i64], i32),
         "kmc_get_config_packed": ([vp, vp, i64], i32),
+        "kmc_vgroup_create_bounds": ([P(KmcGeometry), P(KmcModel), i32, i32, vp, vp, vp], i32),
+        "kmc_workload_mark": ([vp], i32),
+        "kmc_workload_partition": ([vp, i32, i32, vp, vp, vp], i32),
+        "kmc_vgroup_workload_partition": ([vp, i32, i32, i32, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -159,7 +164,7 @@ class KMC:
     """One fractional-step KMC context (kmc_create ... kmc_destroy)."""
 
     def __init__(self, ndim, dims, cell, kind="adsdes", colours=0, replicas=1, seed=0,
-                 rank=0, world=1, device=0, stream=None, nccl_id=None, **params):
+                 rank=0, world=1, device=0, stream=None, nccl_id=None, row_bounds=None, **params):
         self._L = lib()
         self.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
         self.nstates = NSTATES[self.kind]
@@ -172,6 +177,10 @@ class KMC:
             self._id = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
             self.dist.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p)
         self.dist.stream = stream
+        self._bounds = None
+        if row_bounds is not None:       # caller-chosen slabs (kmc_dist.row_bounds, e.g. from workload_partition)
+            self._bounds = np.ascontiguousarray(row_bounds, dtype=np.int64)
+            self.dist.row_bounds = self._bounds.ctypes.data
         self._ctx = ctypes.c_void_p()
         st = self._L.kmc_create(ctypes.byref(self.geom), ctypes.byref(self.model), ctypes.byref(self.dist),
                                 ctypes.byref(self._ctx))
@@ -184,6 +193,7 @@ class KMC:
         self.replica_offset, self.row_offset = ro.value, yo.value
         self.nbytes = rl.value * hl.value * w.value
         qy, qx = (1, int(cell[0])) if int(ndim) == 1 else (int(cell[0]), int(cell[1]))
+        self._strips = int(dims[0]) // qy if int(ndim) == 2 else int(dims[0]) // qx
         # bit-packed layout [plane][cell row][replica][cell column] (kmc_set_config_packed)
         self.packed_shape = (2 if self.nstates == 3 else 1, hl.value // qy, rl.value, w.value // qx)
 
@@ -227,6 +237,16 @@ class KMC:
         out = np.empty(self.packed_shape, dtype=np.uint64)
         self._check(self._L.kmc_get_config_packed(self._ctx, out.ctypes.data, out.size))
         return out
+
+    # ---- f4: workload histogram and cdf re-partition -----------------------------
+    def workload_mark(self):
+        """kmc_workload_mark: the workload interval starts now."""
+        self._check(self._L.kmc_workload_mark(self._ctx))
+
+    def workload_partition(self, parts, granule=1):
+        """kmc_workload_partition: strip loads since the mark and their cdf split into `parts`."""
+        return _partition(self._L, self._check, self._L.kmc_workload_partition, self._ctx, parts, granule,
+                          self._strips)
 
     def set_config_device(self, ptr, nbytes):
         """Device uint8 buffer (e.g. torch CUDA tensor .data_ptr()), stream-ordered."""
@@ -343,12 +363,20 @@ class _Rank(KMC):
         self.nbytes = rl.value * hl.value * w.value
 
 
+def _partition(L, check, fn, ctx, parts, granule, nstrips):
+    bounds = np.zeros(int(parts) + 1, dtype=np.int64)
+    loads = np.zeros(nstrips, dtype=np.uint64)
+    imb = np.zeros(2, dtype=np.float64)
+    check(fn(ctx, int(parts), int(granule), bounds.ctypes.data, loads.ctypes.data, imb.ctypes.data))
+    return {"bounds": bounds, "strip_load": loads, "imbalance": float(imb[0]), "imbalance_even": float(imb[1])}
+
+
 class VGroup:
     """`world` virtual ranks of one 2D lattice on one GPU (kmc_vgroup_*): the multi-GPU slab
     decomposition and halo-exchange protocol, with stream-ordered copies instead of NCCL."""
 
     def __init__(self, world, dims, cell, kind="adsdes", colours=0, replicas=1, seed=0, device=0,
-                 stream=None, **params):
+                 stream=None, row_bounds=None, **params):
         L = lib()
         self._L = L
         self.world = int(world)
@@ -356,8 +384,10 @@ class VGroup:
         self.geom = make_geometry(2, dims, cell, colours, replicas, seed)
         self.model = make_model(k, **params)
         arr = (ctypes.c_void_p * self.world)()
-        st = L.kmc_vgroup_create(ctypes.byref(self.geom), ctypes.byref(self.model), self.world, int(device),
-                                 stream, arr)
+        self._bounds = None if row_bounds is None else np.ascontiguousarray(row_bounds, dtype=np.int64)
+        st = L.kmc_vgroup_create_bounds(ctypes.byref(self.geom), ctypes.byref(self.model), self.world, int(device),
+                                        stream, None if self._bounds is None else self._bounds.ctypes.data, arr)
+        self._strips = int(dims[0]) // int(cell[0])
         if st != KMC_OK:
             raise KmcError(st, L.kmc_create_error().decode())
         self._arr = arr
@@ -389,6 +419,14 @@ class VGroup:
         return self._check(self._L.kmc_vgroup_run_nested(self._arr, self.world, float(T), float(dt), int(n_inner),
                                                          so, si, int(block)),
                            allow=(KMC_WTRUNCATED,)) == KMC_WTRUNCATED
+
+    def workload_mark(self):
+        for rk in self.ranks:
+            self._check(self._L.kmc_workload_mark(rk._ctx))
+
+    def workload_partition(self, parts, granule=1):
+        fn = lambda arr, *rest: self._L.kmc_vgroup_workload_partition(arr, self.world, *rest)
+        return _partition(self._L, self._check, fn, self._arr, parts, granule, self._strips)
 
     def observables(self):
         """Group sum of the integer counters (ghost rows refreshed first)."""

@@ -107,6 +107,10 @@ struct kmc_ctx {
     uint64_t* planes[2] = {nullptr, nullptr};
     long long plane_words = 0;
     uint32_t* wev = nullptr;
+    uint32_t* wmark = nullptr;               // f4: per-cell counters at the last kmc_workload_mark
+    unsigned long long* strips = nullptr;    // f4: strip loads [M strips] + inclusive cdf [M]
+    long long strips_n = 0;
+    long long* wl_out = nullptr;             // f4: device bounds [P+1] + 2 doubles (imbalance)
     unsigned long long* ev_total = nullptr;
     unsigned int* queue = nullptr;           // window kernel's dynamic chunk counter
     unsigned long long* obs_buf = nullptr;   // kObsCounters + 1 (events)
@@ -600,8 +604,22 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     if ((long long)geom->replicas * Mx * My > 0xFFFFFFFFLL)
         return fail(nullptr, KMC_EPARTITION, "more than 2^32 cells in total (Philox counter word)");
     int64_t plan[6];
-    kmc_status ps = kmc_partition_plan(geom, model->kind, world, rank, plan);
-    if (ps != KMC_OK) return ps;
+    if (dist && dist->row_bounds && ndim == 2 && world > 1) {
+        // caller-chosen slabs (f4 re-partition): world+1 cell-row bounds, each slab an even number
+        // (>= 2) of cell rows so the colour pattern stays global
+        const int64_t* b = dist->row_bounds;
+        if (b[0] != 0 || b[world] != My)
+            return fail(nullptr, KMC_EPARTITION, "row_bounds must run from 0 to %lld cell rows", (long long)My);
+        for (int r = 0; r < world; ++r)
+            if (b[r + 1] - b[r] < 2 || (b[r + 1] - b[r]) % 2)
+                return fail(nullptr, KMC_EPARTITION, "row_bounds: slab %d has %lld cell rows (need an even number >= 2)",
+                            r, (long long)(b[r + 1] - b[r]));
+        plan[0] = 0; plan[1] = geom->replicas; plan[2] = b[rank]; plan[3] = b[rank + 1] - b[rank];
+        plan[4] = (rank + world - 1) % world; plan[5] = (rank + 1) % world;
+    } else {
+        kmc_status ps = kmc_partition_plan(geom, model->kind, world, rank, plan);
+        if (ps != KMC_OK) return ps;
+    }
 
     kmc_ctx* c = new kmc_ctx();
     c->geom = *geom;
@@ -661,6 +679,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     bool ok = true;
     for (int p = 0; p < c->nplanes; ++p) ok = ok && alloc((void**)&c->planes[p], (size_t)c->plane_words * 8);
     ok = ok && alloc((void**)&c->wev, (size_t)owned * 4);
+    ok = ok && alloc((void**)&c->wmark, (size_t)owned * 4);
     ok = ok && alloc((void**)&c->ev_total, 8);
     ok = ok && alloc((void**)&c->queue, 8);
     ok = ok && alloc((void**)&c->obs_buf, (kObsCounters + 1) * 8);
@@ -674,6 +693,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     if (!ok) { kmc_destroy(c); return fail(nullptr, KMC_ENOMEM, "device allocation failed (%lld words)", c->plane_words); }
     for (int p = 0; p < c->nplanes; ++p) cudaMemsetAsync(c->planes[p], 0, (size_t)c->plane_words * 8, c->stream);
     cudaMemsetAsync(c->wev, 0, (size_t)owned * 4, c->stream);
+    cudaMemsetAsync(c->wmark, 0, (size_t)owned * 4, c->stream);
     cudaMemsetAsync(c->ev_total, 0, 8, c->stream);
     e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) { kmc_destroy(c); return fail(nullptr, KMC_ECUDA, "init: %s", cudaGetErrorString(e)); }
@@ -701,7 +721,7 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
-    cudaFree(c->wev); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->err_flag);
+    cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv);
     cudaFree(c->spare[0]); cudaFree(c->spare[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);
@@ -914,8 +934,96 @@ kmc_status kmc_run_nested(kmc_ctx* c, double T, double dt, int32_t n_inner, kmc_
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
 
+// ---- f4: workload histogram and cdf re-partition (R29) ----
+static long long strip_count(const kmc_ctx* c) {
+    return c->g.ndim == 2 ? c->geom.dims[0] / c->g.qy : (long long)c->g.Mx;
+}
+
+static kmc_status ensure_strips(kmc_ctx* c, int parts) {
+    const long long M = strip_count(c);
+    if (c->strips_n < M) {
+        cudaFree(c->strips);
+        c->strips = nullptr;
+        if (cudaMalloc((void**)&c->strips, (size_t)M * 16) != cudaSuccess) return fail(c, KMC_ENOMEM, "strip buffers");
+        c->strips_n = M;
+    }
+    if (!c->wl_out && cudaMalloc((void**)&c->wl_out, (size_t)(4096 + 3) * 8) != cudaSuccess)
+        return fail(c, KMC_ENOMEM, "partition output buffer");
+    (void)parts;
+    return KMC_OK;
+}
+
+static kmc_status check_partition_args(kmc_ctx* c, int parts, int granule, const int64_t* bounds) {
+    if (!bounds) return fail(c, KMC_EINVAL, "NULL bounds");
+    const long long M = strip_count(c);
+    if (parts < 1 || parts > 4096) return fail(c, KMC_EINVAL, "parts must be in [1, 4096]");
+    if (granule < 1 || M % granule || M < (long long)parts * granule)
+        return fail(c, KMC_EINVAL, "need strips (%lld) a multiple of granule and >= parts*granule", M);
+    return KMC_OK;
+}
+
+// shared tail: cdf kernel on c's strip buffer, results to the host
+static kmc_status finish_partition(kmc_ctx* c, int parts, int granule, int64_t* bounds, uint64_t* strip_load,
+                                   double* imb) {
+    const long long M = strip_count(c);
+    CUDA_TRY(c, launch_cdf_partition(c->strips, c->strips + M, M, parts, granule, c->wl_out, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(bounds, c->wl_out, (size_t)(parts + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+    double tmp[2];
+    CUDA_TRY(c, cudaMemcpyAsync(tmp, c->wl_out + parts + 1, 16, cudaMemcpyDeviceToHost, c->stream));
+    if (strip_load) CUDA_TRY(c, cudaMemcpyAsync(strip_load, c->strips, (size_t)M * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (imb) { imb[0] = tmp[0]; imb[1] = tmp[1]; }
+    return KMC_OK;
+}
+
+kmc_status kmc_workload_mark(kmc_ctx* c) {
+    if (!c) return KMC_EINVAL;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
+    CUDA_TRY(c, cudaMemcpyAsync(c->wmark, c->wev, owned * 4, cudaMemcpyDeviceToDevice, c->stream));
+    return KMC_OK;
+}
+
+kmc_status kmc_workload_partition(kmc_ctx* c, int32_t parts, int32_t granule, int64_t* bounds, uint64_t* strip_load,
+                                  double* imbalance) {
+    if (!c) return KMC_EINVAL;
+    if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: use kmc_vgroup_workload_partition");
+    kmc_status st = check_partition_args(c, parts, granule, bounds);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    st = ensure_strips(c, parts);
+    if (st != KMC_OK) return st;
+    const long long M = strip_count(c);
+    CUDA_TRY(c, cudaMemsetAsync(c->strips, 0, (size_t)M * 8, c->stream));
+    CUDA_TRY(c, launch_strip_loads(c->g, c->wev, c->wmark, c->strips, c->stream));
+    if (c->world > 1 && c->comm)   // every rank gets the global strip loads, then the same bounds
+        NCCL_TRY(c, g_nccl.AllReduce(c->strips, c->strips, (size_t)M, ncclUint64, ncclSum, c->comm, c->stream));
+    return finish_partition(c, parts, granule, bounds, strip_load, imbalance);
+}
+
+kmc_status kmc_vgroup_workload_partition(kmc_ctx** cs, int32_t world, int32_t parts, int32_t granule, int64_t* bounds,
+                                         uint64_t* strip_load, double* imbalance) {
+    if (!cs || world < 2) return KMC_EINVAL;
+    kmc_ctx* c0 = cs[0];
+    kmc_status st = check_partition_args(c0, parts, granule, bounds);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c0, cudaSetDevice(c0->device));
+    st = ensure_strips(c0, parts);
+    if (st != KMC_OK) return st;
+    const long long M = strip_count(c0);
+    CUDA_TRY(c0, cudaMemsetAsync(c0->strips, 0, (size_t)M * 8, c0->stream));
+    for (int r = 0; r < world; ++r)   // one device, one stream: every rank adds into rank 0's strips
+        CUDA_TRY(c0, launch_strip_loads(cs[r]->g, cs[r]->wev, cs[r]->wmark, c0->strips, c0->stream));
+    return finish_partition(c0, parts, granule, bounds, strip_load, imbalance);
+}
+
 kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, int32_t world, int32_t device,
                              void* stream, kmc_ctx** out) {
+    return kmc_vgroup_create_bounds(geom, model, world, device, stream, nullptr, out);
+}
+
+kmc_status kmc_vgroup_create_bounds(const kmc_geometry* geom, const kmc_model* model, int32_t world, int32_t device,
+                                    void* stream, const int64_t* row_bounds, kmc_ctx** out) {
     if (!geom || !model || !out || world < 2) return fail(nullptr, KMC_EINVAL, "vgroup needs world >= 2");
     if (geom->ndim != 2) return fail(nullptr, KMC_EINVAL, "vgroup: 2D lattices only (1D shards replicas)");
     for (int r = 0; r < world; ++r) out[r] = nullptr;
@@ -935,6 +1043,7 @@ kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, i
     for (int r = 0; r < world; ++r) {
         kmc_dist d{};
         d.rank = r; d.world = world; d.device = device; d.nccl_unique_id = nullptr; d.stream = stream;
+        d.row_bounds = row_bounds;
         kmc_status st = create_ctx(geom, model, &d, true, &out[r]);
         if (st != KMC_OK) {
             for (int q = 0; q < r; ++q) { kmc_destroy(out[q]); out[q] = nullptr; }

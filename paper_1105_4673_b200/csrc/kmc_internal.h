@@ -91,6 +91,10 @@ cudaError_t launch_unpack(const Geo& g, const uint64_t* p0, const uint64_t* p1, 
                           uint8_t* out, cudaStream_t s);
 cudaError_t launch_check_packed(const uint64_t* p0, const uint64_t* p1, long long n, uint64_t valid,
                                 unsigned int* err, cudaStream_t s);
+cudaError_t launch_strip_loads(const Geo& g, const uint32_t* wev, const uint32_t* mark, unsigned long long* strips,
+                               cudaStream_t s);
+cudaError_t launch_cdf_partition(unsigned long long* loads, unsigned long long* cdf, long long M, int P, int granule,
+                                 long long* out, cudaStream_t s);
 cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* a, const uint64_t* b, long long n, cudaStream_t s);
 
 }  // namespace kmc

@@ -562,6 +562,124 @@ cudaError_t launch_unpack(const Geo& g, const uint64_t* p0, const uint64_t* p1, 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// f4: workload histogram (eq.(wload)) per strip and the cdf re-partition (P:919-925,
+// R29).  Strips: cell rows (2D, summed over columns and replicas) or cells (1D, over replicas).
+// W(m) = wev(m) - mark(m) (u32 counters, wrap-safe difference).
+// ---------------------------------------------------------------------------------------------
+__global__ void strip_rows_kernel(const Geo g, const uint32_t* __restrict__ wev, const uint32_t* __restrict__ mark,
+                                  unsigned long long* strips) {
+    // one CTA per owned cell row: the row's R*Mx counters are contiguous
+    const int cy = blockIdx.x;
+    const long long n = (long long)g.R * g.Mx, base = (long long)cy * n;
+    unsigned long long acc = 0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) acc += (uint32_t)(wev[base + i] - mark[base + i]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ unsigned long long part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+        atomicAdd(&strips[g.row_offset + cy], t);
+    }
+}
+
+__global__ void strip_cells_kernel(const Geo g, const uint32_t* __restrict__ wev, const uint32_t* __restrict__ mark,
+                                   unsigned long long* strips) {
+    const int cx = blockIdx.x * blockDim.x + threadIdx.x;          // 1D: one thread per cell, over replicas
+    if (cx >= g.Mx) return;
+    unsigned long long acc = 0;
+    for (int r = 0; r < g.R; ++r) acc += (uint32_t)(wev[(long long)r * g.Mx + cx] - mark[(long long)r * g.Mx + cx]);
+    atomicAdd(&strips[cx], acc);
+}
+
+cudaError_t launch_strip_loads(const Geo& g, const uint32_t* wev, const uint32_t* mark, unsigned long long* strips,
+                               cudaStream_t s) {
+    if (g.ndim == 2) {
+        if (g.My_local > 0) strip_rows_kernel<<<g.My_local, 256, 0, s>>>(g, wev, mark, strips);
+    } else {
+        strip_cells_kernel<<<(g.Mx + 255) / 256, 256, 0, s>>>(g, wev, mark, strips);
+    }
+    return cudaGetLastError();
+}
+
+// R29 rounding of one raw bound to the granule g (nearest multiple, ties up) and clamping
+__device__ __forceinline__ long long round_clamp(long long x, long long prev, int l, int P, long long M, long long gr) {
+    long long r = gr * ((2 * x + gr) / (2 * gr));
+    r = r > prev + gr ? r : prev + gr;
+    const long long hi = M - (long long)(P - l) * gr;
+    return r < hi ? r : hi;
+}
+
+// One CTA: inclusive cdf of the M strip loads (segmented block scan), the P-1 raw bounds by binary
+// search (min s+1 with P*cdf[s] >= l*S), rounding/clamping, and the imbalance (max group load x P / S)
+// of the cdf partition and of the even split.  out = [bounds P+1 (i64)][imb_cdf, imb_even (f64)].
+__global__ void __launch_bounds__(1024) cdf_partition_kernel(unsigned long long* loads, unsigned long long* cdf,
+                                                             long long M, int P, int gr, long long* out) {
+    __shared__ unsigned long long seg_sum[1024];
+    const int t = threadIdx.x, nt = blockDim.x;
+    const long long seg = (M + nt - 1) / nt;
+    const long long a = (long long)t * seg, b = a + seg < M ? a + seg : M;
+    unsigned long long acc = 0;
+    for (long long i = a; i < b; ++i) acc += loads[i];
+    seg_sum[t] = acc;
+    __syncthreads();
+    if (t == 0) {                                   // exclusive scan of the segment sums
+        unsigned long long run = 0;
+        for (int i = 0; i < nt; ++i) { const unsigned long long v = seg_sum[i]; seg_sum[i] = run; run += v; }
+    }
+    __syncthreads();
+    acc = seg_sum[t];
+    for (long long i = a; i < b; ++i) { acc += loads[i]; cdf[i] = acc; }
+    __syncthreads();
+    __threadfence_block();
+    const unsigned long long S = cdf[M - 1];
+    for (int l = 1 + t; l < P; l += nt) {           // raw bounds
+        long long raw;
+        if (S == 0) {
+            raw = ((long long)l * M + P / 2) / P;
+        } else {
+            const unsigned long long thr = (unsigned long long)l * S;
+            long long lo = 0, hi = M - 1;           // min s with P*cdf[s] >= thr (exists: P*S >= thr)
+            while (lo < hi) {
+                const long long mid = (lo + hi) >> 1;
+                if ((unsigned long long)P * cdf[mid] >= thr) hi = mid; else lo = mid + 1;
+            }
+            raw = lo + 1;
+        }
+        out[l] = raw;
+    }
+    __syncthreads();
+    if (t == 0) {
+        auto load = [&](long long x, long long y) -> unsigned long long {
+            return (y > 0 ? cdf[y - 1] : 0ull) - (x > 0 ? cdf[x - 1] : 0ull);
+        };
+        out[0] = 0;
+        long long prev = 0;
+        unsigned long long mx = 0, mx_even = 0, prev_even = 0;
+        for (int l = 1; l <= P; ++l) {
+            const long long bl = l < P ? round_clamp(out[l], prev, l, P, M, gr) : M;
+            const long long be = l < P ? round_clamp(((long long)l * M + P / 2) / P, (long long)prev_even, l, P, M, gr) : M;
+            const unsigned long long g1 = load(prev, bl), g2 = load((long long)prev_even, be);
+            mx = g1 > mx ? g1 : mx;
+            mx_even = g2 > mx_even ? g2 : mx_even;
+            out[l] = bl;
+            prev = bl;
+            prev_even = (unsigned long long)be;
+        }
+        double* imb = reinterpret_cast<double*>(out + P + 1);
+        imb[0] = S ? (double)mx * (double)P / (double)S : 1.0;
+        imb[1] = S ? (double)mx_even * (double)P / (double)S : 1.0;
+    }
+}
+
+cudaError_t launch_cdf_partition(unsigned long long* loads, unsigned long long* cdf, long long M, int P, int granule,
+                                 long long* out, cudaStream_t s) {
+    cdf_partition_kernel<<<1, 1024, 0, s>>>(loads, cdf, M, P, granule, out);
+    return cudaGetLastError();
+}
+
 // validation of a bit-packed slab (kmc_set_config_packed): no bits outside the cell's sites, and in
 // the two-plane models no site both CO and O
 __global__ void check_packed_kernel(const uint64_t* __restrict__ p0, const uint64_t* __restrict__ p1,

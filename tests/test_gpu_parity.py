@@ -448,3 +448,87 @@ def test_packed_config_validation():
     assert np.array_equal(g.get_config(), lat)
     with pytest.raises(ValueError):
         g.set_config_packed(w[:, :1])
+
+
+def _half_full(shape):
+    lat = np.zeros(shape, dtype=np.uint8)
+    lat[:, : shape[1] // 2] = 1                 # top half full: few events; bottom half empty: many
+    return lat
+
+
+@pytest.mark.parametrize("ndim,dims,cell,kind,R,parts,granule", [
+    (2, (128, 64), (8, 8), "adsdes", 2, 4, 2),
+    (2, (64, 32), (4, 4), "zgb", 1, 3, 2),
+    (1, (1024,), (16,), "adsdes", 3, 5, 1),
+])
+def test_workload_partition_matches_oracle(ndim, dims, cell, kind, R, parts, granule):
+    """f4: strip loads since kmc_workload_mark, the cdf bounds and both imbalance figures equal
+    oracle/workload.py applied to the per-cell event counts (eq.(wload), R29)."""
+    from oracle import workload as wk
+    gpu, _ = make_pair(ndim, dims, cell, kind, dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0) if kind == "adsdes" else {}, 0, R)
+    lat = _half_full(gpu.local_shape) if ndim == 2 else si.bernoulli_lattice(gpu.local_shape, 0.3, seed=2)
+    gpu.set_config(lat)
+    gpu.run(1.0, 0.5, "lie")
+    gpu.workload_mark()
+    c0 = gpu.observables(per_cell=True)["per_cell_events"].astype(np.int64)
+    gpu.run(2.0, 0.5, "lie")
+    c1 = gpu.observables(per_cell=True)["per_cell_events"].astype(np.int64)
+    W = (c1 - c0).astype(np.uint64)
+    loads = wk.strip_loads(W, ndim)
+    res = gpu.workload_partition(parts, granule)
+    assert np.array_equal(res["strip_load"], loads)
+    b = wk.cdf_bounds(loads, parts, granule)
+    assert np.array_equal(res["bounds"], b), (res["bounds"], b)
+    assert res["imbalance"] == wk.imbalance(loads, b)
+    assert res["imbalance_even"] == wk.imbalance(loads, wk.even_bounds(len(loads), parts, granule))
+    if ndim == 2 and kind == "adsdes":
+        assert res["imbalance"] < res["imbalance_even"]           # the half-full start is imbalanced
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_rebalanced_slabs_bit_identical(world):
+    """f4 -> a7: the cdf bounds used as kmc_dist.row_bounds (uneven slabs) give the bit-identical
+    lattice and counters of G = 1 and of the even split (global ids); the group's strip loads and
+    bounds equal the single context's."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    dims, cell = (128, 32), (8, 8)
+    p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)
+    one = kmc.KMC(2, dims, cell, kind="adsdes", seed=41, replicas=2, **p)
+    even = kmc.VGroup(world, dims, cell, kind="adsdes", seed=41, replicas=2, **p)
+    lat = _half_full(one.local_shape)
+    one.set_config(lat)
+    even.set_config(lat)
+    one.run(1.0, 0.5, "lie")
+    even.run(1.0, 0.5, "lie")
+    r1 = one.workload_partition(world, 2)
+    rg = even.workload_partition(world, 2)
+    assert np.array_equal(r1["bounds"], rg["bounds"]) and np.array_equal(r1["strip_load"], rg["strip_load"])
+    b = r1["bounds"]
+    assert len(set(np.diff(b))) > 1                                # really uneven
+    reb = kmc.VGroup(world, dims, cell, kind="adsdes", seed=41, replicas=2, row_bounds=b, **p)
+    assert [rk.local_shape[1] // cell[0] for rk in reb.ranks] == list(np.diff(b))
+    reb.set_config(one.get_config())
+    for r in reb.ranks:
+        r.set_state(*one.get_state())
+    for _ in range(2):
+        one.run(1.0, 0.5, "lie")
+        reb.run(1.0, 0.5, "lie")
+        even.run(1.0, 0.5, "lie")
+        assert np.array_equal(one.get_config(), reb.get_config())
+        assert np.array_equal(one.get_config(), even.get_config())
+
+
+def test_workload_partition_errors():
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    g = kmc.KMC(2, (48, 64), (8, 8), kind="adsdes", seed=1)     # 6 strips
+    for parts, gr in [(0, 1), (4, 2), (2, 4), (7, 1)]:
+        with pytest.raises(kmc.KmcError) as e:
+            g.workload_partition(parts, gr)
+        assert e.value.status == 1
+    r = g.workload_partition(3, 2)                                  # no events yet: the even split
+    assert list(r["bounds"]) == [0, 2, 4, 6] and r["imbalance"] == 1.0
+    with pytest.raises(kmc.KmcError) as e:
+        kmc.VGroup(2, (48, 64), (8, 8), kind="adsdes", row_bounds=[0, 3, 6])
+    assert e.value.status == 2

@@ -261,3 +261,32 @@ def test_nested_noninteracting_exact_and_gibbs_invariance():
     pi = pi / pi.sum()
     for Qk in Qc2:
         assert np.abs(pi @ Qk.toarray()).max() < 1e-12
+
+
+def test_workload_cdf_partition_pins():
+    """f4 (P:919-925, R29): closed forms of the cdf re-partition.  Uniform load -> the even split;
+    odd-number loads w_s = 2s+1 (cdf (s+1)^2/M^2) -> b_l = ceil(M sqrt(l/P)); each group's load is
+    at most S/P + max_s w_s (the cdf mapping's defining property); the loads add up to S."""
+    from oracle import workload as wk
+    M, P = 64, 4
+    b = wk.cdf_bounds(np.full(M, 7, dtype=np.uint64), P)
+    assert list(b) == [0, 16, 32, 48, 64]
+    w = np.arange(M, dtype=np.uint64) * 2 + 1
+    b = wk.cdf_bounds(w, P)
+    assert list(b) == [0] + [math.ceil(M * math.sqrt(l / P) - 1e-12) for l in range(1, P)] + [M]
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        w = rng.integers(0, 50, size=96).astype(np.uint64) * (rng.random(96) < 0.7)
+        w[rng.integers(0, 96)] += 500                                   # a hot strip
+        S = int(w.sum())
+        b = wk.cdf_bounds(w, 6)
+        gl = wk.group_loads(w, b)
+        assert int(gl.sum()) == S and np.all(np.diff(b) >= 1)
+        assert gl.max() <= S / 6 + int(w.max())
+    # granule 2: bounds even, every group >= 2 strips, still within the property up to 2 strips
+    w = rng.integers(0, 100, size=128).astype(np.uint64)
+    b = wk.cdf_bounds(w, 8, granule=2)
+    assert np.all(b % 2 == 0) and np.all(np.diff(b) >= 2)
+    assert wk.group_loads(w, b).max() <= w.sum() / 8 + 3 * int(w.max())
+    # no events: the even split
+    assert list(wk.cdf_bounds(np.zeros(12, dtype=np.uint64), 3)) == [0, 4, 8, 12]
