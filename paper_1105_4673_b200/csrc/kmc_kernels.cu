@@ -130,6 +130,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     uint32_t ci = (uint32_t)cbeg64 + lane;
     bool have = ci < cend;
     uint32_t gid32 = 0, k = 0, iCcur = 0;
+    uint32_t wrap = 0;   // hop / pair models: which neighbour indices wrap (W, E, N, S), for the store
     double tclock = 0.0;
     uint64_t P[NP], h[NP][4];
     unsigned long long evsum = 0;
@@ -139,6 +140,8 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         const CellLoc L = locate<NDIM, NEST>(a, c);
         gid32 = L.gid32;
         iCcur = L.iC;
+        if constexpr (KIND != 0)
+            wrap = (L.iW > L.iC ? 1u : 0u) | (L.iE < L.iC ? 2u : 0u) | (L.iN > L.iC ? 4u : 0u) | (L.iS < L.iC ? 8u : 0u);
         k = 0;
         tclock = 0.0;
 #pragma unroll
@@ -157,7 +160,16 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
             evsum += k;
             return;
         }
-        const CellLoc L = locate<NDIM, NEST>(a, c);
+        // neighbour indices from the cell's own index and its wrap bits (no second locate)
+        (void)c;
+        const uint32_t rowlen = (uint32_t)g.R * g.Mx;
+        CellLoc L;
+        L.iC = iCcur;
+        L.iW = (wrap & 1u) ? iCcur + (uint32_t)(g.Mx - 1) : iCcur - 1u;
+        L.iE = (wrap & 2u) ? iCcur - (uint32_t)(g.Mx - 1) : iCcur + 1u;
+        L.iN = (wrap & 4u) ? iCcur + (uint32_t)(g.My_local - 1) * rowlen : iCcur - rowlen;
+        L.iS = (wrap & 8u) ? iCcur - (uint32_t)(g.My_local - 1) * rowlen : iCcur + rowlen;
+        L.iev = iCcur - (uint32_t)g.ghost * rowlen;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             uint64_t* pl = planes[p];
