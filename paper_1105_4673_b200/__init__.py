@@ -13,6 +13,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkmc_b200.so")
+# A/B performance comparisons may point at another in-tree build of the same library
+LIB_PATH = os.environ.get("KMC_B200_LIB", LIB_PATH)
 
 KMC_OK, KMC_EINVAL, KMC_EPARTITION, KMC_ENOMEM, KMC_ECUDA, KMC_ENCCL, KMC_ESTATE = 0, 1, 2, 3, 4, 5, 6
 KMC_WTRUNCATED = 100
