@@ -242,3 +242,47 @@ def test_2d_correlation_long_range_order():
     assert abs((1 - kappa ** 2) ** 0.25 - (2 * exact.paper_cov2d(beta, 1.0) - 1) ** 2) < 1e-12   # M^2 identity
     assert np.all(np.abs(acc[:, 4:] - c2) < 3e-3), (acc[:, 4:] - c2).max()
     assert np.allclose(acc[:, 0], exact.paper_cov2d(beta, 1.0), atol=3e-3)                       # r = 0: coverage
+
+
+@pytest.mark.parametrize("kind,params,cell,scheme,dt,init,bias", [
+    # cfg4 shape: ads/des + diffusion, 4 colours, Strang at dt = 0.1 (P10: bias ~1e-4 there)
+    ("adsdes_diff", dict(ca=1.0, cd=1.0, beta=1.0, K=1.0, h=-2.0, c_hop=1.0), (4, 4), "strang", 0.1, 0.3, 1e-3),
+    # cfg5 shape: ZGB (k1 = 0.4, k2 = 1, R14), empty start, Lie at dt = 0.05
+    ("zgb", dict(k1=0.4, k2=1.0), (4, 4), "lie", 0.05, 0.0, 3e-3),
+])
+def test_gpu_vs_exact_ssa_2d(kind, params, cell, scheme, dt, init, bias):
+    """SURVEY §8(d) cfg4 / cfg5 against O1: species coverages (and the occupied nearest-neighbour
+    pair density) of the GPU fractional-step run vs the exact SSA at T = 0.5, 1, 2 -- within
+    |d| <= 1e-2 and 3 SE + the scheme's splitting bias allowance."""
+    kmc = _kmc()
+    H = W = 64
+    times = [0.5, 1.0, 2.0]
+    Rg, Ro = 256, 64
+    g = kmc.KMC(2, (H, W), cell, kind=kind, replicas=Rg, seed=5, **params)
+    S = g.nstates
+    if init:
+        start = si.bernoulli_lattice((1, H, W), init, seed=31)[0]
+    else:
+        start = np.zeros((H, W), np.uint8)
+    g.set_config(np.broadcast_to(start, (Rg, H, W)).copy())
+
+    def stats(lat):                               # [n][H][W] -> per-lattice observables
+        out = [(lat == s).mean(axis=(1, 2)) for s in range(1, S)]
+        occ = lat == 1
+        out.append((occ & np.roll(occ, -1, axis=2)).mean(axis=(1, 2)) + (occ & np.roll(occ, -1, axis=1)).mean(axis=(1, 2)))
+        return np.stack(out, axis=1)
+
+    gpu, t = [], 0.0
+    for T in times:
+        g.run(T - t, dt, scheme)
+        t = T
+        gpu.append(stats(g.get_config()))
+    o1 = [ssa_snapshots(start, 2, kind, model_params(**params), times, seed=13, stream=r)[0] for r in range(Ro)]
+    for i, T in enumerate(times):
+        a = gpu[i]
+        b = stats(np.stack([o[i] for o in o1]))
+        for j in range(a.shape[1]):
+            d = a[:, j].mean() - b[:, j].mean()
+            se = math.sqrt(a[:, j].var(ddof=1) / Rg + b[:, j].var(ddof=1) / Ro)
+            assert abs(d) <= 1e-2, (kind, T, j, d)
+            assert abs(d) <= 3 * se + bias, (kind, T, j, d, se)
