@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared",
            "-I", INCLUDE, "-I", nccl_include(), "-Xptxas", "-v" if verbose else "-O3",
-           "-o", LIB + ".tmp"] + sources() + ["-ldl"]
+           "-o", LIB + ".tmp"] + sources() + ["-ldl"] + os.environ.get("KMC_NVCC_FLAGS", "").split()
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
