@@ -225,6 +225,14 @@ kmc_status kmc_vgroup_create(const kmc_geometry* geom, const kmc_model* model, i
                              void* stream, kmc_ctx** out);
 kmc_status kmc_vgroup_run(kmc_ctx** ctxs, int32_t world, double T, double dt, kmc_scheme scheme);
 kmc_status kmc_vgroup_sync(kmc_ctx** ctxs, int32_t world);
+/* Fused halo exchange on a virtual-rank group (the exchange folded into the window
+ * kernel): enable != 0 makes every rank's window kernel mirror each write to a word of its first /
+ * last owned cell row into the neighbour slab's ghost row, and each halo-delta XOR into a ghost row
+ * into the neighbour's owned row (peer pointers to the other slabs' planes), so kmc_vgroup_run
+ * performs no exchange between windows (one ghost refresh at the start of each call).  Results are
+ * bit-identical to the exchange protocol and to world = 1.  Nested runs keep the exchange path.
+ * While enabled, configuration uploads copy into the planes instead of swapping buffers. */
+kmc_status kmc_vgroup_set_fused(kmc_ctx** ctxs, int32_t world, int32_t enable);
 /* kmc_run_nested on a virtual-rank group (one exchange per outer factor). */
 kmc_status kmc_vgroup_run_nested(kmc_ctx** ctxs, int32_t world, double T, double dt, int32_t n_inner,
                                  kmc_scheme outer, kmc_scheme inner, int32_t block);

@@ -32,6 +32,7 @@ EXPORTS = [
     "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale", "kmc_run_nested",
     "kmc_vgroup_run_nested", "kmc_set_config_packed", "kmc_get_config_packed",
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
+    "kmc_vgroup_set_fused",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -113,8 +114,12 @@ def lib():
         "kmc_workload_mark": ([vp], i32),
         "kmc_workload_partition": ([vp, i32, i32, vp, vp, vp], i32),
         "kmc_vgroup_workload_partition": ([vp, i32, i32, i32, vp, vp, vp], i32),
+        "kmc_vgroup_set_fused": ([vp, i32, i32], i32),
     }
+    ab_build = "KMC_B200_LIB" in os.environ          # an older build under comparison may lack new entry points
     for name, (args, res) in sig.items():
+        if ab_build and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -421,6 +426,10 @@ class VGroup:
         return self._check(self._L.kmc_vgroup_run_nested(self._arr, self.world, float(T), float(dt), int(n_inner),
                                                          so, si, int(block)),
                            allow=(KMC_WTRUNCATED,)) == KMC_WTRUNCATED
+
+    def set_fused(self, enable=True):
+        """kmc_vgroup_set_fused: the halo exchange folded into the window kernels (peer writes)."""
+        self._check(self._L.kmc_vgroup_set_fused(self._arr, self.world, int(bool(enable))))
 
     def workload_mark(self):
         for rk in self.ranks:

@@ -108,6 +108,10 @@ struct kmc_ctx {
     long long plane_words = 0;
     uint32_t* wev = nullptr;
     uint32_t* wmark = nullptr;               // f4: per-cell counters at the last kmc_workload_mark
+    bool fused = false;                      // fused halo exchange (peer writes inside the window kernel)
+    uint64_t* peer_up[2] = {nullptr, nullptr};
+    uint64_t* peer_dn[2] = {nullptr, nullptr};
+    int peer_up_rows = 0;
     unsigned long long* strips = nullptr;    // f4: strip loads [M strips] + inclusive cdf [M]
     long long strips_n = 0;
     long long* wl_out = nullptr;             // f4: device bounds [P+1] + 2 doubles (imbalance)
@@ -357,6 +361,10 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     a.colour = colour;
     a.D = D;
     const long long nactive = nest ? apply_nest(c, *nest, a) : active_cells(c);
+    if (c->fused && !nest) {
+        for (int p = 0; p < 2; ++p) { a.peer_up[p] = c->peer_up[p]; a.peer_dn[p] = c->peer_dn[p]; }
+        a.peer_up_rows = c->peer_up_rows;
+    }
     // refill batching of the window kernel (performance only; results are bit-identical): a warp
     // refills its finished lanes once refill_min of them are parked.  Best thresholds measured on
     // B200 (tools/sweep_refill.sh) depend on the expected events per cell-window mu ~ D x
@@ -746,6 +754,18 @@ kmc_status kmc_local_shape(const kmc_ctx* c, int64_t* rl, int64_t* hl, int64_t* 
     return KMC_OK;
 }
 
+// A validated configuration in the spare planes becomes the lattice.  Normally a pointer swap; with
+// the fused exchange the plane buffers are mapped by the neighbour ranks, so they must stay put.
+static kmc_status swap_in_spare(kmc_ctx* c) {
+    for (int p = 0; p < c->nplanes; ++p) {
+        if (c->fused)
+            CUDA_TRY(c, cudaMemcpyAsync(c->planes[p], c->spare[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
+        else
+            std::swap(c->spare[p], c->planes[p]);
+    }
+    return KMC_OK;
+}
+
 static long long slab_bytes(const kmc_ctx* c) { return (long long)c->g.R * c->H_local * c->W; }
 
 static kmc_status ensure_staging(kmc_ctx* c) {
@@ -791,8 +811,7 @@ kmc_status kmc_set_config(kmc_ctx* c, const uint8_t* host, int64_t nbytes) {
     CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->err_flag, 4, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (*c->h_err) return fail(c, KMC_EINVAL, "spin value >= %d in the configuration", c->nstates);
-    for (int p = 0; p < c->nplanes; ++p) std::swap(c->spare[p], c->planes[p]);
-    return KMC_OK;
+    return swap_in_spare(c);
 }
 
 kmc_status kmc_get_config(kmc_ctx* c, uint8_t* host, int64_t nbytes) {
@@ -831,8 +850,7 @@ kmc_status kmc_set_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nword
     CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->err_flag, 4, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (*c->h_err) return fail(c, KMC_EINVAL, "packed configuration has bits outside the cells or a site both CO and O");
-    for (int p = 0; p < c->nplanes; ++p) std::swap(c->spare[p], c->planes[p]);
-    return KMC_OK;
+    return swap_in_spare(c);
 }
 
 kmc_status kmc_get_config_packed(kmc_ctx* c, uint64_t* host, int64_t nwords) {
@@ -1055,6 +1073,25 @@ kmc_status kmc_vgroup_create_bounds(const kmc_geometry* geom, const kmc_model* m
     return KMC_OK;
 }
 
+kmc_status kmc_vgroup_set_fused(kmc_ctx** cs, int32_t world, int32_t enable) {
+    if (!cs || world < 2) return KMC_EINVAL;
+    for (int r = 0; r < world; ++r)
+        if (!cs[r] || !cs[r]->vgroup || cs[r]->world != world || cs[r]->rank != r)
+            return fail(cs[0], KMC_EINVAL, "vgroup: contexts must be ranks 0..world-1 of one kmc_vgroup_create");
+    for (int r = 0; r < world; ++r) {
+        kmc_ctx* c = cs[r];
+        kmc_ctx* up = cs[c->rank_up];
+        kmc_ctx* dn = cs[c->rank_down];
+        c->fused = enable != 0;
+        for (int p = 0; p < 2; ++p) {
+            c->peer_up[p] = enable ? up->planes[p] : nullptr;
+            c->peer_dn[p] = enable ? dn->planes[p] : nullptr;
+        }
+        c->peer_up_rows = up->g.My_local;
+    }
+    return KMC_OK;
+}
+
 kmc_status kmc_vgroup_sync(kmc_ctx** cs, int32_t world) {
     if (!cs || world < 2) return KMC_EINVAL;
     CUDA_TRY(cs[0], cudaSetDevice(cs[0]->device));
@@ -1071,11 +1108,16 @@ kmc_status kmc_vgroup_run(kmc_ctx** cs, int32_t world, double T, double dt, kmc_
     if (scheme < KMC_LIE || scheme > KMC_RANDOM) return fail(c0, KMC_EINVAL, "unknown scheme %d", (int)scheme);
     CUDA_TRY(c0, cudaSetDevice(c0->device));
     bool truncated = false;
+    const bool fused = c0->fused;
+    if (fused) {   // ghost rows current once; afterwards the window kernels keep them current
+        kmc_status st = vgroup_forward(cs, world);
+        if (st != KMC_OK) return st;
+    }
     for (double d : macro_durations(T, dt, &truncated)) {
         for (const auto& sd : macro_schedule(scheme, c0->C, d, c0->geom.seed, c0->window)) {
-            kmc_status st = vgroup_forward(cs, world);
+            kmc_status st = fused ? KMC_OK : vgroup_forward(cs, world);
             for (int r = 0; r < world && st == KMC_OK; ++r) st = launch_window(cs[r], sd.first, sd.second);
-            if (st == KMC_OK) st = vgroup_reverse(cs, world);
+            if (st == KMC_OK && !fused) st = vgroup_reverse(cs, world);
             if (st != KMC_OK) return st;
         }
         for (int r = 0; r < world; ++r) cs[r]->time += d;

@@ -59,6 +59,13 @@ struct SubstepArgs {
     double log_c[kLogTab];           // log_spec tables: c_j = 128/(j+91)
     double log_l[kLogTab];           //   L_j = -log(c_j), host libm
     double lcoef[6];                 //   {1/7, -1/6, 1/5, 1/3, ln2_hi, ln2_lo} (exact hex literals)
+    // fused halo exchange (SURVEY §8(e) "later option"): the window kernel mirrors every write to a
+    // boundary-row or ghost-row word into the neighbour ranks' planes (peer pointers: other slabs on
+    // the same device, or CUDA-IPC mappings of a peer GPU's planes over NVLink), so no separate
+    // exchange runs between windows.  peer_up[0] == nullptr: off.
+    uint64_t* peer_up[2];
+    uint64_t* peer_dn[2];
+    int peer_up_rows;                // the up neighbour's owned cell rows (its last row / bottom ghost)
 };
 
 struct ObsArgs {

@@ -37,6 +37,7 @@ namespace kmc {
 // ---------------------------------------------------------------------------------------------
 struct CellLoc {
     uint32_t iC, iW, iE, iN, iS;      // word indices of the cell and its 4 neighbours (one plane)
+    uint32_t sy;                      // storage row of the cell (owned rows are 1..My_local with ghosts)
     uint32_t iev;                     // index into the per-cell event counters
     uint32_t gid32;                   // global cell id (Philox counter word 1, R17)
 };
@@ -89,6 +90,7 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     const uint32_t rbase = r * g.Mx;
     const uint32_t base = (uint32_t)sy * rowlen + rbase;
     CellLoc L;
+    L.sy = (uint32_t)sy;
     L.iC = base + cx;
     L.iW = base + cxW;
     L.iE = base + cxE;
@@ -100,7 +102,26 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     return L;
 }
 
-template <int KIND, int NDIM, int BS, int MINB, bool MH, bool NEST>
+// Fused exchange (PEER): mirror a modification of word `col` of storage row `row` into the
+// neighbour slabs.  Rows: 0 = top ghost (= up's last owned row), 1 = first owned (= up's bottom
+// ghost), My = last owned (= down's top ghost), My+1 = bottom ghost (= down's first owned row).
+// Full-word stores go to ghost copies (no other writer of that word in this window); XOR deltas are
+// system-scope atomics (the target may sit in a peer GPU's memory).
+__device__ __forceinline__ void mirror_word(const SubstepArgs& a, int p, uint32_t row, uint32_t col, uint64_t v,
+                                            bool is_xor) {
+    const uint32_t rowlen = (uint32_t)a.g.R * a.g.Mx;
+    const uint32_t My = (uint32_t)a.g.My_local, Mu = (uint32_t)a.peer_up_rows;
+    uint64_t* tgt = nullptr;
+    if (row == 0) tgt = a.peer_up[p] + (size_t)Mu * rowlen + col;
+    else if (row == 1) tgt = a.peer_up[p] + (size_t)(Mu + 1) * rowlen + col;
+    else if (row == My) tgt = a.peer_dn[p] + col;
+    else if (row == My + 1) tgt = a.peer_dn[p] + (size_t)rowlen + col;
+    if (!tgt) return;
+    if (is_xor) atomicXor_system((unsigned long long*)tgt, (unsigned long long)v);
+    else *tgt = v;
+}
+
+template <int KIND, int NDIM, int BS, int MINB, bool MH, bool NEST, bool PEER>
 __global__ void __launch_bounds__(BS, MINB)
 substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
     using M = Model<KIND, NDIM>;
@@ -131,6 +152,8 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     bool have = ci < cend;
     uint32_t gid32 = 0, k = 0, iCcur = 0;
     uint32_t wrap = 0;   // hop / pair models: which neighbour indices wrap (W, E, N, S), for the store
+    uint32_t srow = 0;   // PEER: storage row of the current cell
+    bool peer_wrote = false;
     double tclock = 0.0;
     uint64_t P[NP], h[NP][4];
     unsigned long long evsum = 0;
@@ -140,6 +163,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         const CellLoc L = locate<NDIM, NEST>(a, c);
         gid32 = L.gid32;
         iCcur = L.iC;
+        if constexpr (PEER) srow = L.sy;
         if constexpr (KIND != 0)
             wrap = (L.iW > L.iC ? 1u : 0u) | (L.iE < L.iC ? 2u : 0u) | (L.iN > L.iC ? 4u : 0u) | (L.iS < L.iC ? 8u : 0u);
         k = 0;
@@ -156,6 +180,13 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         if (k == 0) return;
         if constexpr (KIND == 0) {   // spin flip writes only its own word: no second locate
             planes[0][iCcur] = P[0];
+            if constexpr (PEER) {
+                const uint32_t rl = (uint32_t)g.R * g.Mx;
+                if (srow == 1 || srow == (uint32_t)g.My_local) {
+                    mirror_word(a, 0, srow, iCcur - srow * rl, P[0], false);
+                    peer_wrote = true;
+                }
+            }
             atomicAdd(&a.wev[iCcur - (uint32_t)g.ghost * ((uint32_t)g.R * g.Mx)], k);
             evsum += k;
             return;
@@ -184,11 +215,26 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
                 const uint64_t dE = hE ^ ((pl[L.iE] << (g.qx - 1)) & g.colL);
                 if (dW) atomicXor((unsigned long long*)&pl[L.iW], (unsigned long long)(dW << (g.qx - 1)));
                 if (dE) atomicXor((unsigned long long*)&pl[L.iE], (unsigned long long)(dE >> (g.qx - 1)));
+                uint64_t dN = 0, dS = 0;
                 if (NDIM == 2) {
-                    const uint64_t dN = hN ^ ((pl[L.iN] >> g.shN) & g.row0);
-                    const uint64_t dS = hS ^ ((pl[L.iS] << g.shN) & g.rowL);
+                    dN = hN ^ ((pl[L.iN] >> g.shN) & g.row0);
+                    dS = hS ^ ((pl[L.iS] << g.shN) & g.rowL);
                     if (dN) atomicXor((unsigned long long*)&pl[L.iN], (unsigned long long)(dN << g.shN));
                     if (dS) atomicXor((unsigned long long*)&pl[L.iS], (unsigned long long)(dS >> g.shN));
+                }
+                if constexpr (PEER) {   // rows 0 / 1 / My / My+1 are shared with a neighbour slab
+                    const uint32_t My = (uint32_t)g.My_local;
+                    const uint32_t col = iCcur - srow * rowlen;
+                    if (srow <= 2 || srow + 1 >= My) {
+                        if (srow == 1 || srow == My) {
+                            mirror_word(a, p, srow, col, P[p], false);
+                            if (dW) mirror_word(a, p, srow, L.iW - srow * rowlen, dW << (g.qx - 1), true);
+                            if (dE) mirror_word(a, p, srow, L.iE - srow * rowlen, dE >> (g.qx - 1), true);
+                        }
+                        if (dN) mirror_word(a, p, srow - 1, col, dN << g.shN, true);
+                        if (dS) mirror_word(a, p, srow + 1, col, dS >> g.shN, true);
+                        peer_wrote = true;
+                    }
                 }
             }
         }
@@ -237,6 +283,9 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
             if (!__any_sync(FULL, have)) break;
         }
     }
+    if constexpr (PEER) {
+        if (peer_wrote) __threadfence_system();                    // peer writes visible before the signal
+    }
     // event total: warp-aggregated
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) evsum += __shfl_xor_sync(FULL, evsum, o);
@@ -253,10 +302,10 @@ static int resident_ctas(K kernel, int bs) {
     return per * nsm;
 }
 
-template <int KIND, int NDIM, int MINB, bool MH, bool NEST>
+template <int KIND, int NDIM, int MINB, bool MH, bool NEST, bool PEER = false>
 static cudaError_t launch_v(const SubstepArgs& a, long long nactive, cudaStream_t s) {
     constexpr int bs = 256;
-    auto kern = substep_kernel<KIND, NDIM, bs, MINB, MH, NEST>;
+    auto kern = substep_kernel<KIND, NDIM, bs, MINB, MH, NEST, PEER>;
     // persistent grid: one wave of resident warps, each starting on its own chunk of 32*8 cells
     static int cap = 0;                                            // per instantiation
     if (cap == 0) cap = resident_ctas(kern, bs);
@@ -287,6 +336,7 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
         // spin flip: the four separate (window-constant) halo boards save 8 logic ops per event and
         // measured 3 % faster at dt = 1; <= 64 registers (no spills) -> 4 CTAs of 256 per SM
         if (a.nest) return launch_v<KIND, NDIM, 4, false, true>(a, nactive, s);
+        if (NDIM == 2 && a.peer_up[0]) return launch_v<KIND, NDIM, 4, false, false, NDIM == 2>(a, nactive, s);
         if (mh_ok && mh_env == 1) return launch_v<KIND, NDIM, 3, true, false>(a, nactive, s);
         if (lb == 6) return launch_v<KIND, NDIM, 3, false, false>(a, nactive, s);
         return launch_v<KIND, NDIM, 4, false, false>(a, nactive, s);
@@ -298,6 +348,9 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
         const bool big = (KIND == 1 && lb != 4) || lb == 3;
         if (a.nest) return big ? launch_v<KIND, NDIM, 2, true, true>(a, nactive, s)
                                : launch_v<KIND, NDIM, 3, true, true>(a, nactive, s);
+        if (NDIM == 2 && a.peer_up[0])
+            return big ? launch_v<KIND, NDIM, 2, true, false, NDIM == 2>(a, nactive, s)
+                       : launch_v<KIND, NDIM, 3, true, false, NDIM == 2>(a, nactive, s);
         return big ? launch_v<KIND, NDIM, 2, true, false>(a, nactive, s)
                    : launch_v<KIND, NDIM, 3, true, false>(a, nactive, s);
     }

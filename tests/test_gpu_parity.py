@@ -532,3 +532,44 @@ def test_workload_partition_errors():
     with pytest.raises(kmc.KmcError) as e:
         kmc.VGroup(2, (48, 64), (8, 8), kind="adsdes", row_bounds=[0, 3, 6])
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("kind,params,cell,scheme,dt", [
+    ("adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), (8, 8), "lie", 1.0),
+    ("adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), (4, 4), "strang", 0.5),
+    ("zgb", dict(k1=0.45, k2=1.0), (2, 4), "random", 0.5),
+    ("zgb_diff", dict(k1=0.4, k2=1.0, c_hop=0.8), (4, 2), "lie", 0.25),
+])
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_exchange_bit_identical(kind, params, cell, scheme, dt, world):
+    """SURVEY §8(e) fused exchange: window kernels that mirror their boundary-row writes and ghost-row
+    XOR deltas straight into the neighbour slabs (no exchange between windows) give the lattice,
+    event counts and observables of G = 1, also across a configuration upload mid-run and with
+    uneven slabs."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    dims = (64, 32)
+    qy = cell[0]
+    rows = dims[0] // qy
+    bounds = None
+    if world == 2:                                   # uneven slabs as well
+        bounds = [0, 2 * (rows // 8), rows]
+    one = kmc.KMC(2, dims, cell, kind=kind, seed=37, replicas=2, **params)
+    grp = kmc.VGroup(world, dims, cell, kind=kind, seed=37, replicas=2, row_bounds=bounds, **params)
+    grp.set_fused(True)
+    lat = (si.bernoulli_lattice(one.local_shape, 0.5, seed=5) if not kind.startswith("zgb")
+           else si.categorical_lattice(one.local_shape, [0.5, 0.25, 0.25], seed=5))
+    one.set_config(lat)
+    grp.set_config(lat)
+    for i in range(3):
+        one.run(2 * dt, dt, scheme)
+        grp.run(2 * dt, dt, scheme)
+        assert np.array_equal(one.get_config(), grp.get_config()), i
+        if i == 1:                                   # upload mid-run: planes must stay in place
+            lat2 = one.get_config()
+            one.set_config(lat2)
+            grp.set_config(lat2)
+    a, b = one.observables(), grp.observables()
+    assert a["events"] == b["events"] > 0
+    for key in ("n_state", "nn_pairs", "n_state_by_colour"):
+        assert np.array_equal(a[key], b[key]), key

@@ -7,7 +7,7 @@ import subprocess
 import sys
 import tempfile
 
-want = sys.argv[1] if len(sys.argv) > 1 else "_ZN3kmc14substep_kernelILi0ELi2ELi256ELi4ELb0ELb0EEEvNS_11SubstepArgsEjj"
+want = sys.argv[1] if len(sys.argv) > 1 else "_ZN3kmc14substep_kernelILi0ELi2ELi256ELi4ELb0ELb0ELb0EEEvNS_11SubstepArgsEjj"
 cubin_name = sys.argv[2] if len(sys.argv) > 2 else "kmc_kernels.sm_100a.cubin"
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath("paper_1105_4673_b200/libkmc_b200.so")], cwd=d,

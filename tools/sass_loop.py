@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 lib = "paper_1105_4673_b200/libkmc_b200.so"
-want = sys.argv[1] if len(sys.argv) > 1 else "ILi0ELi2ELi256ELi4ELb0ELb0E"
+want = sys.argv[1] if len(sys.argv) > 1 else "ILi0ELi2ELi256ELi4ELb0ELb0ELb0E"
 out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s*Function : ", out)
 for f in funcs:
