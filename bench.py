@@ -98,7 +98,7 @@ def cpu_baseline_sample(wl, seconds_hint="~10-30 s"):
                       f"macro-steps dt={wl['dt']}, {o.events} events in {el:.1f} s, 1 thread"}
 
 
-def arm_config(workload, dt, world):
+def arm_config(workload, dt, world, fused=False):
     """The `config` object of both arms (the workload the metric is quoted on)."""
     wl = si.WORKLOADS[workload]
     C = 2 if (wl["ndim"] == 1 or wl["kind"] == "adsdes") else 4
@@ -106,7 +106,9 @@ def arm_config(workload, dt, world):
             "model": wl["kind"], "params": wl["params"], "scheme": wl["scheme"], "dt": dt,
             "init": f"Bernoulli({wl['init']})", "colours": C,
             "l2": "inputs larger than L2 (bit-packed lattice 128 MiB/GPU at 32768^2 > 126 MB L2)",
-            "parallelism": f"slab{world}" if wl["ndim"] == 2 else f"replicas{world}"}
+            "parallelism": (f"slab{world}" if wl["ndim"] == 2 else f"replicas{world}"),
+            "exchange": ("fused (peer writes in the window kernel)" if fused else "nccl send/recv")
+                        if wl["ndim"] == 2 and world > 1 else "none"}
 
 
 def run_reference(args):
@@ -151,6 +153,8 @@ def main():
     ap.add_argument("--dt", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--fused-exchange", action="store_true",
+                    help="N > 1: halo exchange folded into the window kernel (CUDA IPC + device flags)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -182,7 +186,7 @@ def main():
     stream = torch.cuda.current_stream()
     k = kmc.KMC(ndim, gdims, wl["cell"], kind=wl["kind"], replicas=wl.get("replicas", world if ndim == 1 else 1),
                 seed=0xB200, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=uid,
-                **wl["params"])
+                fused_exchange=args.fused_exchange and world > 1, **wl["params"])
     shape = k.local_shape
     if wl["kind"].startswith("zgb"):
         lat = si.categorical_lattice(shape, [1.0 - wl["init"], wl["init"] / 2, wl["init"] / 2] if wl["init"] else [1.0, 0.0, 0.0],
@@ -307,7 +311,7 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
         "data": "synthetic",
-        "config": arm_config(args.workload, dt, world),
+        "config": arm_config(args.workload, dt, world, args.fused_exchange),
         "site_updates_per_s": site_updates,
         "events_per_step": events / args.steps,
         "roofline": roof,

@@ -89,6 +89,12 @@ typedef struct {
                                      [b_r, b_{r+1}), each an even number >= 2; e.g. from
                                      kmc_workload_partition), NULL = the even split.  Results do not depend
                                      on the split (global ids).  KMC_EPARTITION if invalid. */
+    int32_t fused_exchange;       /* 2D, world > 1: 1 = fold the halo exchange into the window kernel (SURVEY
+                                     §8(e)): the neighbours' planes are mapped with CUDA IPC (NVLink peer
+                                     memory, one process per GPU on one node), the kernel writes the shared
+                                     rows directly and windows are ordered by device-side flags instead of
+                                     NCCL send/recv; bit-identical results.  0 = NCCL exchange (default).
+                                     KMC_ECUDA if the IPC setup fails. */
 } kmc_dist;
 
 typedef struct {

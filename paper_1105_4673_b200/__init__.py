@@ -50,7 +50,8 @@ class KmcGeometry(ctypes.Structure):
 
 class KmcDist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("row_bounds", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("row_bounds", ctypes.c_void_p),
+                ("fused_exchange", ctypes.c_int32)]
 
 
 class KmcObs(ctypes.Structure):
@@ -171,7 +172,8 @@ class KMC:
     """One fractional-step KMC context (kmc_create ... kmc_destroy)."""
 
     def __init__(self, ndim, dims, cell, kind="adsdes", colours=0, replicas=1, seed=0,
-                 rank=0, world=1, device=0, stream=None, nccl_id=None, row_bounds=None, **params):
+                 rank=0, world=1, device=0, stream=None, nccl_id=None, row_bounds=None, fused_exchange=False,
+                 **params):
         self._L = lib()
         self.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
         self.nstates = NSTATES[self.kind]
@@ -184,6 +186,7 @@ class KMC:
             self._id = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
             self.dist.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p)
         self.dist.stream = stream
+        self.dist.fused_exchange = 1 if fused_exchange else 0
         self._bounds = None
         if row_bounds is not None:       # caller-chosen slabs (kmc_dist.row_bounds, e.g. from workload_partition)
             self._bounds = np.ascontiguousarray(row_bounds, dtype=np.int64)

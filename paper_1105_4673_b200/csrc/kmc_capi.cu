@@ -38,6 +38,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -60,6 +61,7 @@ bool load_nccl(std::string* why) {
     LOADSYM(GroupStart, "ncclGroupStart");
     LOADSYM(GroupEnd, "ncclGroupEnd");
     LOADSYM(AllReduce, "ncclAllReduce");
+    LOADSYM(AllGather, "ncclAllGather");
     LOADSYM(GetErrorString, "ncclGetErrorString");
 #undef LOADSYM
     g_nccl.ok = true;
@@ -109,6 +111,12 @@ struct kmc_ctx {
     uint32_t* wev = nullptr;
     uint32_t* wmark = nullptr;               // f4: per-cell counters at the last kmc_workload_mark
     bool fused = false;                      // fused halo exchange (peer writes inside the window kernel)
+    bool fused_ipc = false;                  // ... across GPUs: CUDA-IPC peer planes + device flags
+    unsigned long long* flags = nullptr;     // [2]: written by the up / down neighbour
+    unsigned long long* peer_up_flags = nullptr;
+    unsigned long long* peer_dn_flags = nullptr;
+    unsigned long long epoch = 0;            // fused windows completed
+    std::vector<void*> ipc_open;             // IPC mappings to close at destroy
     uint64_t* peer_up[2] = {nullptr, nullptr};
     uint64_t* peer_dn[2] = {nullptr, nullptr};
     int peer_up_rows = 0;
@@ -408,9 +416,26 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     return KMC_OK;
 }
 
+// Fused exchange across GPUs: the ghost rows are refreshed by one NCCL exchange at the start of every
+// call that runs windows (configuration uploads may have changed the neighbours' rows); afterwards
+// the window kernels keep them current.  Every rank makes the same calls, so this stays collective.
+kmc_status fused_refresh(kmc_ctx* c) {
+    return c->fused_ipc ? exchange_forward(c) : KMC_OK;
+}
+
 kmc_status do_substep(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull) {
     if (colour < 0 || colour >= c->C) return fail(c, KMC_EINVAL, "colour %d out of range [0,%d)", colour, c->C);
     if (!(D >= 0.0)) return fail(c, KMC_EINVAL, "window duration must be >= 0");
+    if (c->fused_ipc) {
+        // fused exchange across GPUs: wait for both neighbours' previous window, run the window
+        // (its kernel writes the neighbours' shared rows through NVLink), signal completion
+        CUDA_TRY(c, launch_wait_flags(c->flags, c->epoch, c->stream));
+        kmc_status st = launch_window(c, colour, D, class_mask);
+        if (st != KMC_OK) return st;
+        ++c->epoch;
+        CUDA_TRY(c, launch_signal_flags(c->peer_up_flags, c->peer_dn_flags, c->epoch, c->stream));
+        return KMC_OK;
+    }
     kmc_status st = exchange_forward(c);
     if (st != KMC_OK) return st;
     st = launch_window(c, colour, D, class_mask);
@@ -579,6 +604,63 @@ kmc_status kmc_create(const kmc_geometry* geom, const kmc_model* model, const km
 
 }  // extern "C"
 
+// Fused exchange across GPUs (kmc_dist.fused_exchange): every rank exports its plane buffers and a
+// 2-word flag array as CUDA-IPC handles; an NCCL all-gather gives every rank its ring neighbours'
+// handles and slab heights; the neighbours' planes and flags are mapped into this process (NVLink
+// peer memory).  The window kernel then writes the shared rows directly (PEER variant) and
+// do_substep orders windows with the device flags instead of NCCL send/recv.
+static bool setup_fused_ipc(kmc_ctx* c, std::string* why) {
+    struct Blob { cudaIpcMemHandle_t planes[2]; cudaIpcMemHandle_t flags; long long rows; };
+    auto ck = [&](cudaError_t e, const char* what) {
+        if (e != cudaSuccess) { *why = std::string(what) + ": " + cudaGetErrorString(e); return false; }
+        return true;
+    };
+    if (!ck(cudaMalloc((void**)&c->flags, 16), "flags") || !ck(cudaMemset(c->flags, 0, 16), "flags")) return false;
+    Blob mine{};
+    for (int p = 0; p < c->nplanes; ++p)
+        if (!ck(cudaIpcGetMemHandle(&mine.planes[p], c->planes[p]), "cudaIpcGetMemHandle(plane)")) return false;
+    if (!ck(cudaIpcGetMemHandle(&mine.flags, c->flags), "cudaIpcGetMemHandle(flags)")) return false;
+    mine.rows = c->g.My_local;
+    // planes must never be reallocated or swapped from now on (set_config copies, see swap_in_spare)
+    for (int p = 0; p < c->nplanes; ++p)
+        if (!c->spare[p] && !ck(cudaMalloc((void**)&c->spare[p], (size_t)c->plane_words * 8), "spare planes")) return false;
+    uint8_t* dsend = nullptr;
+    uint8_t* drecv = nullptr;
+    if (!ck(cudaMalloc((void**)&dsend, sizeof(Blob)), "blob") ||
+        !ck(cudaMalloc((void**)&drecv, sizeof(Blob) * (size_t)c->world), "blobs")) { cudaFree(dsend); return false; }
+    std::vector<Blob> all((size_t)c->world);
+    bool ok = ck(cudaMemcpy(dsend, &mine, sizeof(Blob), cudaMemcpyHostToDevice), "blob upload");
+    if (ok) {
+        const ncclResult_t r = g_nccl.AllGather(dsend, drecv, sizeof(Blob), ncclUint8, c->comm, c->stream);
+        if (r != ncclSuccess) { *why = std::string("ncclAllGather: ") + g_nccl.GetErrorString(r); ok = false; }
+    }
+    ok = ok && ck(cudaStreamSynchronize(c->stream), "all-gather");
+    ok = ok && ck(cudaMemcpy(all.data(), drecv, sizeof(Blob) * (size_t)c->world, cudaMemcpyDeviceToHost), "blob download");
+    cudaFree(dsend);
+    cudaFree(drecv);
+    if (!ok) return false;
+    auto open = [&](const cudaIpcMemHandle_t& hnd, void** ptr) {
+        return ck(cudaIpcOpenMemHandle(ptr, hnd, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle") &&
+               (c->ipc_open.push_back(*ptr), true);
+    };
+    const Blob& up = all[(size_t)c->rank_up];
+    const Blob& dn = all[(size_t)c->rank_down];
+    void* ptr = nullptr;
+    for (int p = 0; p < c->nplanes; ++p) {
+        if (!open(up.planes[p], &ptr)) return false;
+        c->peer_up[p] = (uint64_t*)ptr;
+        if (c->rank_down == c->rank_up) c->peer_dn[p] = c->peer_up[p];   // world 2: one mapping
+        else { if (!open(dn.planes[p], &ptr)) return false; c->peer_dn[p] = (uint64_t*)ptr; }
+    }
+    if (!open(up.flags, &ptr)) return false;
+    c->peer_up_flags = (unsigned long long*)ptr;
+    if (c->rank_down == c->rank_up) c->peer_dn_flags = c->peer_up_flags;
+    else { if (!open(dn.flags, &ptr)) return false; c->peer_dn_flags = (unsigned long long*)ptr; }
+    c->peer_up_rows = (int)up.rows;
+    c->fused = c->fused_ipc = true;
+    return true;
+}
+
 static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, const kmc_dist* dist, bool vgroup,
                              kmc_ctx** out) {
     if (!out) return fail(nullptr, KMC_EINVAL, "NULL out");
@@ -716,6 +798,10 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
         memcpy(&id, dist->nccl_unique_id, 128);
         ncclResult_t r = g_nccl.CommInitRank(&c->comm, world, id, rank);
         if (r != ncclSuccess) { kmc_destroy(c); return fail(nullptr, KMC_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)); }
+        if (dist->fused_exchange && ndim == 2) {
+            std::string why2;
+            if (!setup_fused_ipc(c, &why2)) { kmc_destroy(c); return fail(nullptr, KMC_ECUDA, "fused exchange setup: %s", why2.c_str()); }
+        }
     }
     *out = c;
     return KMC_OK;
@@ -727,8 +813,10 @@ void kmc_destroy(kmc_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
+    cudaFree(c->flags);
     cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv);
     cudaFree(c->spare[0]); cudaFree(c->spare[1]);
@@ -869,6 +957,8 @@ kmc_status kmc_substep(kmc_ctx* c, int32_t colour, double duration) {
     if (!c) return KMC_EINVAL;
     if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: use kmc_vgroup_run");
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st = fused_refresh(c);
+    if (st != KMC_OK) return st;
     return do_substep(c, colour, duration);
 }
 
@@ -878,6 +968,8 @@ kmc_status kmc_run(kmc_ctx* c, double T, double dt, kmc_scheme scheme) {
     if (scheme < KMC_LIE || scheme > KMC_RANDOM) return fail(c, KMC_EINVAL, "unknown scheme %d", (int)scheme);
     if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: use kmc_vgroup_run");
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st0 = fused_refresh(c);
+    if (st0 != KMC_OK) return st0;
     bool truncated = false;
     for (double d : macro_durations(T, dt, &truncated)) {
         for (const auto& sd : macro_schedule(scheme, c->C, d, c->geom.seed, c->window)) {
@@ -905,6 +997,8 @@ kmc_status kmc_run_multiscale(kmc_ctx* c, double T, double dt, int32_t n_fast, k
         return fail(c, KMC_EINVAL, "multiscale needs a non-empty proper subset of fast classes");
     const uint64_t slow = all & ~fast_classes;
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st0 = fused_refresh(c);
+    if (st0 != KMC_OK) return st0;
     bool truncated = false;
     for (double d : macro_durations(T, dt, &truncated)) {
         // eq.(strang3): e^{d/2 L_r} [e^{(d/N) L_f}]^N e^{d/2 L_r}, each factor split over colours

@@ -102,6 +102,9 @@ cudaError_t launch_strip_loads(const Geo& g, const uint32_t* wev, const uint32_t
                                cudaStream_t s);
 cudaError_t launch_cdf_partition(unsigned long long* loads, unsigned long long* cdf, long long M, int P, int granule,
                                  long long* out, cudaStream_t s);
+cudaError_t launch_wait_flags(const unsigned long long* flags, unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_signal_flags(unsigned long long* up_flags, unsigned long long* dn_flags, unsigned long long v,
+                                cudaStream_t s);
 cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* a, const uint64_t* b, long long n, cudaStream_t s);
 
 }  // namespace kmc

@@ -745,6 +745,44 @@ cudaError_t launch_cdf_partition(unsigned long long* loads, unsigned long long* 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fused exchange across GPUs: per-window neighbour synchronisation through flags in device memory
+// (each rank's flags[0] is written by its up neighbour, flags[1] by its down neighbour, through
+// CUDA-IPC mappings over NVLink).  A rank may start window e only when both neighbours have
+// finished window e-1 (their peer writes into this rank are complete, and they no longer read the
+// rows this window will write).  One thread; a stuck neighbour traps after ~2^35 cycles instead of
+// hanging the stream.
+// ---------------------------------------------------------------------------------------------
+__global__ void wait_flags_kernel(const unsigned long long* flags, unsigned long long epoch) {
+    const long long t0 = clock64();
+    for (;;) {
+        unsigned long long a, b;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(flags));
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(b) : "l"(flags + 1));
+        if (a >= epoch && b >= epoch) return;
+        if (clock64() - t0 > (1ll << 35)) __trap();
+        __nanosleep(200);
+    }
+}
+
+__global__ void signal_flags_kernel(unsigned long long* up_flags, unsigned long long* dn_flags, unsigned long long v) {
+    __threadfence_system();
+    // I am my up neighbour's down neighbour (its flags[1]) and my down neighbour's up neighbour
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(up_flags + 1), "l"(v) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(dn_flags), "l"(v) : "memory");
+}
+
+cudaError_t launch_wait_flags(const unsigned long long* flags, unsigned long long epoch, cudaStream_t s) {
+    wait_flags_kernel<<<1, 1, 0, s>>>(flags, epoch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_signal_flags(unsigned long long* up_flags, unsigned long long* dn_flags, unsigned long long v,
+                                cudaStream_t s) {
+    signal_flags_kernel<<<1, 1, 0, s>>>(up_flags, dn_flags, v);
+    return cudaGetLastError();
+}
+
 // validation of a bit-packed slab (kmc_set_config_packed): no bits outside the cell's sites, and in
 // the two-plane models no site both CO and O
 __global__ void check_packed_kernel(const uint64_t* __restrict__ p0, const uint64_t* __restrict__ p1,
