@@ -273,6 +273,10 @@ kmc_status kmc_nccl_unique_id(uint8_t out[128]);
 /* Library version string. */
 const char* kmc_version(void);
 
+/* ABI check (host only, no device): out[0..3] = sizeof(kmc_geometry), sizeof(kmc_model),
+ * sizeof(kmc_dist), sizeof(kmc_obs), so bindings can verify their struct layouts. */
+void kmc_abi_sizes(int64_t out[4]);
+
 #ifdef __cplusplus
 }
 #endif

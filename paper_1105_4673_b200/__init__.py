@@ -32,7 +32,7 @@ EXPORTS = [
     "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale", "kmc_run_nested",
     "kmc_vgroup_run_nested", "kmc_set_config_packed", "kmc_get_config_packed",
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
-    "kmc_vgroup_set_fused",
+    "kmc_vgroup_set_fused", "kmc_abi_sizes",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -116,6 +116,7 @@ def lib():
         "kmc_workload_partition": ([vp, i32, i32, vp, vp, vp], i32),
         "kmc_vgroup_workload_partition": ([vp, i32, i32, i32, vp, vp, vp], i32),
         "kmc_vgroup_set_fused": ([vp, i32, i32], i32),
+        "kmc_abi_sizes": ([vp], None),
     }
     ab_build = "KMC_B200_LIB" in os.environ          # an older build under comparison may lack new entry points
     for name, (args, res) in sig.items():

@@ -561,6 +561,14 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
 extern "C" {
 
 const char* kmc_version(void) { return KMC_VERSION; }
+
+void kmc_abi_sizes(int64_t out[4]) {
+    if (!out) return;
+    out[0] = (int64_t)sizeof(kmc_geometry);
+    out[1] = (int64_t)sizeof(kmc_model);
+    out[2] = (int64_t)sizeof(kmc_dist);
+    out[3] = (int64_t)sizeof(kmc_obs);
+}
 const char* kmc_create_error(void) { return g_create_error.c_str(); }
 const char* kmc_last_error(const kmc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
 

@@ -67,3 +67,11 @@ def test_partition_plan_slabs_and_ring():
         kmc.partition_plan(2, (256, 64), (8, 8), 1, "adsdes", 3, 0)    # 32 cell rows / 3 ranks
     with pytest.raises(kmc.KmcError):
         kmc.partition_plan(2, (64, 64), (8, 8), 1, "adsdes", 8, 0)     # 1 cell row per rank (< 2)
+
+
+def test_struct_layouts_match_the_header():
+    """The ctypes mirrors of kmc_geometry / kmc_model / kmc_dist / kmc_obs have the C sizes."""
+    out = (ctypes.c_int64 * 4)()
+    kmc.lib().kmc_abi_sizes(out)
+    assert list(out) == [ctypes.sizeof(kmc.KmcGeometry), ctypes.sizeof(kmc.KmcModel),
+                         ctypes.sizeof(kmc.KmcDist), ctypes.sizeof(kmc.KmcObs)]
