@@ -90,7 +90,7 @@ def cpu_baseline_sample(wl, seconds_hint="~10-30 s"):
     o = FSKMC(wl["ndim"], (side, side), wl["cell"], wl["kind"], model_params(**wl["params"]), seed=7)
     o.set_config(si.bernoulli_lattice((1, side, side), wl["init"], seed=si.SEED_BASE + 1))
     t0 = time.perf_counter()
-    nmacro = 2
+    nmacro = 4                                         # ~15 s of single-thread oracle work
     o.run(nmacro * wl["dt"], wl["dt"], wl["scheme"])
     el = time.perf_counter() - t0
     return {"value": o.events / el, "unit": UNIT, "cores": 1, "kind": "oracle",
