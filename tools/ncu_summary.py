@@ -66,10 +66,29 @@ def main():
     d, stalls = read_raw(a.rep)
     b = json.loads(open(a.bench).read().strip().splitlines()[-1])
     C = b["config"].get("colours", 2)
-    ev_launch = b["events_per_step"] / C
-    ipe = d["warp_inst"] / ev_launch
+    lps = {"lie": C, "strang": 2 * C - 1, "random": C}[b["config"].get("scheme", "lie")]   # windows per step
+    ev_launch = b["events_per_step"] / lps
+    ipe = d["warp_inst"] / ev_launch            # the captured launch against the mean launch
+    ipe_src = "captured launch / mean events per launch"
+    # preferred: instructions summed over the timed steps' launches (launch list with
+    # smsp__inst_executed.sum) / the events of those steps -- exact for schedules whose windows
+    # differ in duration (Strang half steps)
+    if a.launches and os.path.exists(a.launches):
+        per = {}
+        for r in csv.reader(open(a.launches)):
+            if len(r) > 14 and r[0].isdigit() and "substep_kernel" in r[4] and r[12] == "smsp__inst_executed.sum":
+                per[int(r[0])] = float(r[14].replace(",", ""))
+        if per:
+            ids = sorted(per)
+            warm, steps = b.get("warmup", 3), b.get("steps", 2)
+            timed = ids[warm * lps:(warm + steps) * lps]
+            if len(timed) == steps * lps:
+                ipe = sum(per[i] for i in timed) / (b["events_per_step"] * steps)
+                ipe_src = f"launch list: instructions of the {len(timed)} timed launches / their events"
+    ipe_note = ipe_src
     summary = {
         "warp_inst_per_event": round(ipe, 3),
+        "warp_inst_per_event_source": ipe_note,
         "thread_inst_per_event": round(ipe * d.get("threads_per_inst", 32), 1),
         "events_per_launch": ev_launch,
         "dram_bytes_per_launch": d.get("dram_read", 0) + d.get("dram_write", 0),
@@ -95,7 +114,8 @@ def main():
     md += ["", "Warp stall reasons (warps stalled per issued instruction):", ""]
     md += [f"- {k}: {v}" for k, v in summary["stalls_per_issue"].items()]
     if a.launches and os.path.exists(a.launches):
-        rows = [r for r in csv.reader(open(a.launches)) if len(r) > 14 and r[0].isdigit()]
+        rows = [r for r in csv.reader(open(a.launches)) if len(r) > 14 and r[0].isdigit()
+                and r[12] == "gpu__time_duration.sum"]
         tot = {}
         for r in rows:
             name = r[4].split("(")[0].replace("void ", "")

@@ -8,7 +8,7 @@ for spec in ${@:-ising2d_32768:adsdes zgb2d_32768:zgb diff2d_8192:adsdes_diff}; 
   timeout 300 $CMD --workload $w > gpurun_out/plain_$kind.log 2> gpurun_out/plain_$kind.err; rc=$?
   echo "$w plain rc=$rc"
   [ $rc -ne 0 ] && continue
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none --csv \
       --log-file gpurun_out/launches_$kind.csv $CMD --workload $w > /dev/null 2>&1
   echo "$w launches rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:substep -s 6 -c 1 \
