@@ -290,7 +290,10 @@ def main():
         prof = json.load(open(os.path.join(ROOT, "profiles", "substep_profile.json")))
     except Exception:
         pass
-    ipe = prof.get(wl["kind"], {}).get("warp_inst_per_event")
+    # the per-unit figure must come from an ncu capture of this workload at this dt
+    pkey = wl["kind"] if dt == wl["dt"] else f"{wl['kind']}@dt{dt:g}"
+    pent = prof.get(pkey, {})
+    ipe = pent.get("warp_inst_per_event") if pent.get("workload") == args.workload else None
     sm_clk = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     issue_peak = 148 * 4 * sm_clk * 1e6 / 1e9                              # G warp-inst / s
     achieved = ipe * events_per_launch / (avg_launch_ms / 1e3) / 1e9 if ipe else None
@@ -298,7 +301,8 @@ def main():
             "frac": (achieved / issue_peak) if achieved else None,
             "peak_source": f"148 SMs x 4 schedulers x 1 warp-inst/clk x {sm_clk:.0f} MHz (median SM clock under load)",
             "per_unit": f"{ipe} warp-inst/event (ncu sm__inst_executed / events, profiles/substep_profile.json)",
-            "traffic": prof.get(wl["kind"], {}).get("dram_bytes_per_launch"),
+            "traffic": pent.get("dram_bytes_per_launch") if ipe else None,
+            "profile_key": pkey if ipe else None,
             "kernel": "substep_kernel", "avg_launch_ms": avg_launch_ms, "launches": launches,
             "kernel_share_of_step": kern_ms / ms,
             "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],

@@ -3,8 +3,10 @@
 # Usage: bash tools/profile.sh [workload[:kind] ...]   outputs under gpurun_out/
 mkdir -p gpurun_out
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
-for spec in ${@:-ising2d_32768:adsdes zgb2d_32768:zgb diff2d_8192:adsdes_diff}; do
-  w=${spec%%:*}; kind=${spec#*:}
+for spec in ${@:-ising2d_32768:adsdes zgb2d_32768:zgb diff2d_8192:adsdes_diff ising2d_32768:adsdes:0.01}; do
+  w=${spec%%:*}; rest=${spec#*:}; kind=${rest%%:*}; dt=${rest#*:}; [ "$dt" = "$rest" ] && dt=""
+  [ -n "$dt" ] && kind="$kind@dt$dt"
+  CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 ${dt:+--dt $dt}"
   timeout 300 $CMD --workload $w > gpurun_out/plain_$kind.log 2> gpurun_out/plain_$kind.err; rc=$?
   echo "$w plain rc=$rc"
   [ $rc -ne 0 ] && continue
