@@ -98,11 +98,16 @@ def cpu_baseline_sample(wl, seconds_hint="~10-30 s"):
                       f"macro-steps dt={wl['dt']}, {o.events} events in {el:.1f} s, 1 thread"}
 
 
-def arm_config(workload, dt, world, fused=False):
+def arm_config(workload, dt, world, fused=False, scaling="weak"):
     """The `config` object of both arms (the workload the metric is quoted on)."""
     wl = si.WORKLOADS[workload]
     C = 2 if (wl["ndim"] == 1 or wl["kind"] == "adsdes") else 4
-    return {"workload": workload, "dims_per_gpu": list(wl["dims"]), "cell": list(wl["cell"]),
+    dims = list(wl["dims"])
+    if scaling == "strong" and wl["ndim"] == 2:
+        per_gpu, global_dims = [dims[0] // world, dims[1]], dims
+    else:
+        per_gpu, global_dims = dims, ([dims[0] * world, dims[1]] if wl["ndim"] == 2 else dims)
+    return {"workload": workload, "dims_per_gpu": per_gpu, "global_dims": global_dims, "cell": list(wl["cell"]),
             "model": wl["kind"], "params": wl["params"], "scheme": wl["scheme"], "dt": dt,
             "init": f"Bernoulli({wl['init']})", "colours": C,
             "l2": "inputs larger than L2 (bit-packed lattice 128 MiB/GPU at 32768^2 > 126 MB L2)",
@@ -135,9 +140,10 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64",
         "data": "synthetic",
-        "config": arm_config(args.workload, args.dt if args.dt is not None else wl["dt"], args.gpus),
+        "config": arm_config(args.workload, args.dt if args.dt is not None else wl["dt"], args.gpus,
+                             False, args.scaling),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -153,6 +159,8 @@ def main():
     ap.add_argument("--dt", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: one workload-sized slab per GPU (default); strong: the workload split over the GPUs")
     ap.add_argument("--fused-exchange", action="store_true",
                     help="N > 1: halo exchange folded into the window kernel (CUDA IPC + device flags)")
     args = ap.parse_args()
@@ -178,9 +186,11 @@ def main():
     wl = dict(si.WORKLOADS[args.workload])
     dt = args.dt if args.dt is not None else wl["dt"]
     ndim = wl["ndim"]
+    strong = args.scaling == "strong"
     if ndim == 2:
         H1, W = wl["dims"]
-        gdims = (H1 * world, W)          # weak scaling: one H1 x W slab per GPU
+        # weak scaling: one H1 x W slab per GPU; strong: the H1 x W lattice split over the GPUs
+        gdims = (H1, W) if strong else (H1 * world, W)
     else:
         gdims = wl["dims"]
     stream = torch.cuda.current_stream()
@@ -313,9 +323,9 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64",
         "data": "synthetic",
-        "config": arm_config(args.workload, dt, world, args.fused_exchange),
+        "config": arm_config(args.workload, dt, world, args.fused_exchange, args.scaling),
         "site_updates_per_s": site_updates,
         "events_per_step": events / args.steps,
         "roofline": roof,
