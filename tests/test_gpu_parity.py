@@ -569,6 +569,13 @@ def test_fused_exchange_bit_identical(kind, params, cell, scheme, dt, world):
             lat2 = one.get_config()
             one.set_config(lat2)
             grp.set_config(lat2)
+    if (dims[0] // qy) % 4 == 0 and all(rk.local_shape[1] // qy % 2 == 0 for rk in grp.ranks):
+        one.run_nested(1.0, 0.5, 2, "lie", "lie", 2)   # nested runs keep the exchange path
+        grp.run_nested(1.0, 0.5, 2, "lie", "lie", 2)
+        assert np.array_equal(one.get_config(), grp.get_config())
+        one.run(2 * dt, dt, scheme)                  # and fused windows resume after them
+        grp.run(2 * dt, dt, scheme)
+        assert np.array_equal(one.get_config(), grp.get_config())
     a, b = one.observables(), grp.observables()
     assert a["events"] == b["events"] > 0
     for key in ("n_state", "nn_pairs", "n_state_by_colour"):
