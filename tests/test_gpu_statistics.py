@@ -286,3 +286,33 @@ def test_gpu_vs_exact_ssa_2d(kind, params, cell, scheme, dt, init, bias):
             se = math.sqrt(a[:, j].var(ddof=1) / Rg + b[:, j].var(ddof=1) / Ro)
             assert abs(d) <= 1e-2, (kind, T, j, d)
             assert abs(d) <= 3 * se + bias, (kind, T, j, d, se)
+
+
+def test_2d_ising_transient_vs_exact_ssa():
+    """North star in 2D (target parameters beta = 1.5, h_dyn = -2, 8x8 cells, 64^2): the coverage
+    transient from a fixed Bernoulli(1/2) lattice (it dips to ~0.36 before relaxing towards 1/2)
+    against the exact SSA.  Strang at the paper's dt = 1 and Lie at dt = 0.5 stay within 1e-2
+    (and 3 SE + 5e-3 of splitting bias); Lie at dt = 1 has the larger transient bias (measured
+    ~1.3e-2 at T = 1, a property of the method), which shrinks with dt."""
+    kmc = _kmc()
+    p = dict(ca=1.0, cd=1.0, beta=1.5, K=1.0, h=-2.0)
+    H, times, Rg, Ro = 64, [1.0, 2.0, 5.0], 512, 96
+    start = si.bernoulli_lattice((1, H, H), 0.5, seed=31)[0]
+    o1 = np.array([[s.mean() for s in ssa_snapshots(start, 2, "adsdes", model_params(**p), times, seed=13,
+                                                     stream=r)[0]] for r in range(Ro)])
+    d = {}
+    for scheme, dt in (("strang", 1.0), ("lie", 0.5), ("lie", 1.0)):
+        g = kmc.KMC(2, (H, H), (8, 8), kind="adsdes", replicas=Rg, seed=5, **p)
+        g.set_config(np.broadcast_to(start, (Rg, H, H)).copy())
+        t = 0.0
+        for i, T in enumerate(times):
+            g.run(T - t, dt, scheme)
+            t = T
+            a = g.get_config().reshape(Rg, -1).mean(axis=1)
+            b = o1[:, i]
+            d[(scheme, dt, T)] = a.mean() - b.mean()
+            se = math.sqrt(a.var(ddof=1) / Rg + b.var(ddof=1) / Ro)
+            if (scheme, dt) != ("lie", 1.0):
+                assert abs(d[(scheme, dt, T)]) <= 1e-2, (scheme, dt, T, d[(scheme, dt, T)])
+                assert abs(d[(scheme, dt, T)]) <= 3 * se + 5e-3, (scheme, dt, T, d[(scheme, dt, T)], se)
+    assert abs(d[("lie", 1.0, 1.0)]) > abs(d[("lie", 0.5, 1.0)]) + 3e-3, d      # the Lie bias shrinks with dt
