@@ -107,3 +107,36 @@ def test_c_example_runs(tmp_path):
     # from Bernoulli(1/2) the Arrhenius kinetics first dip to ~0.39 (the exact SSA shows the same
     # transient) before relaxing towards the zero-field value 1/2
     assert 0.3 < cov < 0.6 and 0 < ev[0] < ev[1] < ev[2]
+
+
+def test_product_and_oracle_share_no_code():
+    """The CUDA product (paper_1105_4673_b200/) never imports or includes oracle/, and oracle/ never
+    imports, includes or links the product; synth_inputs.py (shared seeded inputs) imports neither."""
+    import ast
+
+    def py_imports(path):
+        tree = ast.parse(open(path).read())
+        mods = set()
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Import):
+                mods |= {a.name.split(".")[0] for a in node.names}
+            elif isinstance(node, ast.ImportFrom) and node.module:
+                mods.add(node.module.split(".")[0])
+        return mods
+
+    prod = os.path.join(ROOT, "paper_1105_4673_b200")
+    for f in os.listdir(prod):
+        if f.endswith(".py"):
+            assert "oracle" not in py_imports(os.path.join(prod, f)), f
+    for f in os.listdir(os.path.join(prod, "csrc")):
+        src = open(os.path.join(prod, "csrc", f)).read()
+        assert not re.search(r'#include\s+"[^"]*oracle', src), f
+    orc = os.path.join(ROOT, "oracle")
+    for f in os.listdir(orc):
+        p = os.path.join(orc, f)
+        if f.endswith(".py"):
+            assert "paper_1105_4673_b200" not in py_imports(p), f
+        if f.endswith(".c"):
+            src = open(p).read()
+            assert not re.search(r'#include\s+"', src), f          # only system headers
+    assert py_imports(os.path.join(ROOT, "synth_inputs.py")) <= {"numpy"}
