@@ -140,3 +140,12 @@ def test_product_and_oracle_share_no_code():
             src = open(p).read()
             assert not re.search(r'#include\s+"', src), f          # only system headers
     assert py_imports(os.path.join(ROOT, "synth_inputs.py")) <= {"numpy"}
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without the CUDA library every entry point raises."""
+    code = ("import paper_1105_4673_b200 as k\n"
+            "try:\n    k.KMC(2, (16, 16), (4, 4))\nexcept ImportError as e:\n    print('raised', e)\n")
+    env = dict(os.environ, KMC_B200_LIB=str(tmp_path / "missing.so"), PYTHONPATH=ROOT)
+    r = subprocess.run(["python", "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    assert "raised" in r.stdout, (r.stdout, r.stderr)
