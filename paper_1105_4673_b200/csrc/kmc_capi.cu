@@ -820,6 +820,9 @@ extern "C" {
 void kmc_destroy(kmc_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    // fused exchange across GPUs: the neighbours' last windows write into our rows; wait for their
+    // completion signals before the buffers go away
+    if (c->fused_ipc && c->flags && c->stream) launch_wait_flags(c->flags, c->epoch, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
