@@ -190,6 +190,36 @@ kmc_status kmc_observables(kmc_ctx* ctx, kmc_obs* out, uint32_t* per_cell_events
  * Synchronous; the counts are exact integers. */
 kmc_status kmc_correlation(kmc_ctx* ctx, int32_t rmax, int32_t state, int64_t* out_x, int64_t* out_y);
 
+/* The coverage process C_t = |Lambda|^-1 sum_x 1{sigma_t(x) = state} of each replica (SURVEY §8(f)
+ * f1; Figs. path1D, autocorr1D, pdf2d, dynamics2d: sample paths, autocorrelation function and
+ * equilibrium distribution of the coverage; reading R30).
+ *
+ * kmc_record_coverage: (re)start recording.  Sample 0 is taken now; kmc_run, kmc_run_multiscale,
+ *   kmc_run_nested and kmc_vgroup_run(_nested) append one sample at the end of every macro-step
+ *   (including a shortened last one), on the device, stream-ordered, no host synchronisation.
+ *   A sample is the per-LOCAL-replica number of sites in `state` (0 .. nstates-1) over the owned
+ *   cells.  At most `capacity` samples are kept (later ones are dropped); capacity = 0 stops
+ *   recording and frees the buffer.  KMC_EINVAL for a bad state or capacity < 0, KMC_ENOMEM.
+ * kmc_coverage_series: copies min(max_samples, n) samples to `out` (host int64, [sample][local
+ *   replica]) and sets *n_samples = n (out may be NULL to query n).  World > 1 over NCCL in 2D:
+ *   the counts are summed over the rank slabs (complete per replica); 1D ranks own whole replicas.
+ *   Virtual-rank contexts return their own slab's partial counts.  Synchronous.
+ * kmc_coverage_stats: statistics of samples [first, n) over ALL replicas (all ranks), with
+ *   c = count / sites-per-replica, M = replicas, n' = n - first:
+ *     moments[0] = mean  c_bar = sum c / (M n');  moments[1] = gamma(0)
+ *     gamma(l)   = sum_r sum_{i=first}^{n-1-l} (c_{i,r} - c_bar)(c_{i+l,r} - c_bar) / (M (n' - l))
+ *     acf[l]     = gamma(l) / gamma(0) for l = 0..max_lag (all 0 when gamma(0) = 0)
+ *     hist[b]    = #{(i, r) : floor(count_{i,r} * bins / (N + 1)) = b}, b < bins, N = sites per
+ *                  replica (bins = N + 1: the exact distribution of N C_t)
+ *   acf, moments, hist are host arrays (max_lag+1, 2, bins entries) and may each be NULL.
+ *   KMC_EINVAL unless 0 <= first < n, 0 <= max_lag < n - first and (hist NULL or 1 <= bins <= N+1);
+ *   KMC_ESTATE on a virtual-rank context.  Lag l is l macro-steps.  Synchronous; collective over
+ *   NCCL ranks (every rank must call it). */
+kmc_status kmc_record_coverage(kmc_ctx* ctx, int32_t state, int64_t capacity);
+kmc_status kmc_coverage_series(kmc_ctx* ctx, int64_t* out, int64_t max_samples, int64_t* n_samples);
+kmc_status kmc_coverage_stats(kmc_ctx* ctx, int64_t first, int32_t max_lag, double* acf, double* moments,
+                              int32_t bins, int64_t* hist);
+
 /* Checkpoint / resume: the whole state is (lattice, window counter, time, seed, config). */
 kmc_status kmc_get_state(const kmc_ctx* ctx, uint64_t* windows, double* time);
 kmc_status kmc_set_state(kmc_ctx* ctx, uint64_t windows, double time);

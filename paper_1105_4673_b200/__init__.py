@@ -32,7 +32,7 @@ EXPORTS = [
     "kmc_set_kernel", "kmc_correlation", "kmc_run_multiscale", "kmc_run_nested",
     "kmc_vgroup_run_nested", "kmc_set_config_packed", "kmc_get_config_packed",
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
-    "kmc_vgroup_set_fused", "kmc_abi_sizes",
+    "kmc_vgroup_set_fused", "kmc_abi_sizes", "kmc_record_coverage", "kmc_coverage_series", "kmc_coverage_stats",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -117,6 +117,9 @@ def lib():
         "kmc_vgroup_workload_partition": ([vp, i32, i32, i32, vp, vp, vp], i32),
         "kmc_vgroup_set_fused": ([vp, i32, i32], i32),
         "kmc_abi_sizes": ([vp], None),
+        "kmc_record_coverage": ([vp, i32, i64], i32),
+        "kmc_coverage_series": ([vp, vp, i64, P(i64)], i32),
+        "kmc_coverage_stats": ([vp, i64, i32, vp, vp, i32, vp], i32),
     }
     ab_build = "KMC_B200_LIB" in os.environ          # an older build under comparison may lack new entry points
     for name, (args, res) in sig.items():
@@ -323,6 +326,30 @@ class KMC:
         oy = np.zeros(int(rmax) + 1, dtype=np.int64)
         self._check(self._L.kmc_correlation(self._ctx, int(rmax), int(state), ox.ctypes.data, oy.ctypes.data))
         return {"x": ox, "y": oy}
+
+    def record_coverage(self, capacity, state=1):
+        """Start recording the coverage process (kmc_record_coverage): sample 0 now, then one per
+        macro-step of run / run_multiscale / run_nested (capacity 0 stops and frees)."""
+        self._check(self._L.kmc_record_coverage(self._ctx, int(state), int(capacity)))
+
+    def coverage_series(self):
+        """Recorded samples (kmc_coverage_series): int64 [n][local replicas] site counts."""
+        n = ctypes.c_int64()
+        self._check(self._L.kmc_coverage_series(self._ctx, None, 0, ctypes.byref(n)))
+        out = np.zeros((int(n.value), self.local_shape[0]), dtype=np.int64)
+        if out.size:
+            self._check(self._L.kmc_coverage_series(self._ctx, out.ctypes.data, out.shape[0], ctypes.byref(n)))
+        return out
+
+    def coverage_stats(self, max_lag, first=0, bins=0):
+        """kmc_coverage_stats over samples [first, n): {'mean', 'var' (= gamma(0)), 'acf'
+        float64[max_lag+1], 'hist' int64[bins] (bins > 0)}."""
+        acf = np.zeros(int(max_lag) + 1, dtype=np.float64)
+        mom = np.zeros(2, dtype=np.float64)
+        hist = np.zeros(int(bins), dtype=np.int64) if bins else None
+        self._check(self._L.kmc_coverage_stats(self._ctx, int(first), int(max_lag), acf.ctypes.data, mom.ctypes.data,
+                                               int(bins), hist.ctypes.data if bins else None))
+        return {"mean": float(mom[0]), "var": float(mom[1]), "acf": acf, "hist": hist}
 
     def get_state(self):
         w, t = ctypes.c_uint64(), ctypes.c_double()

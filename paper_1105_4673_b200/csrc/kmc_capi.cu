@@ -8,6 +8,7 @@
 #include "kmc_internal.h"
 #include "../../include/kmc.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -124,6 +125,9 @@ struct kmc_ctx {
     long long strips_n = 0;
     long long* wl_out = nullptr;             // f4: device bounds [P+1] + 2 doubles (imbalance)
     unsigned long long* ev_total = nullptr;
+    unsigned long long* series = nullptr;    // f1 coverage process: [series_cap][R local] counts (R30)
+    long long series_cap = 0, series_n = 0;
+    int series_state = 1;
     unsigned int* queue = nullptr;           // window kernel's dynamic chunk counter
     unsigned long long* obs_buf = nullptr;   // kObsCounters + 1 (events)
     unsigned int* err_flag = nullptr;
@@ -242,6 +246,24 @@ long long active_cells(const kmc_ctx* c) {
 }
 
 // a7 forward exchange (world > 1, 2D): owned boundary cell rows -> neighbours' ghost rows.
+// f1 (R30): append one sample of the coverage process (per-replica count of series_state over the
+// owned cells) to the device series; stream-ordered, no host synchronisation.  Full: no-op.
+kmc_status record_sample(kmc_ctx* c) {
+    if (!c->series || c->series_n >= c->series_cap) return KMC_OK;
+    unsigned long long* out = c->series + (size_t)c->series_n * c->g.R;
+    CUDA_TRY(c, cudaMemsetAsync(out, 0, (size_t)c->g.R * 8, c->stream));
+    SeriesArgs a{};
+    a.g = c->g;
+    a.plane0 = c->planes[0];
+    a.plane1 = c->planes[1];
+    a.nplanes = c->nplanes;
+    a.state = c->series_state;
+    a.out = out;
+    CUDA_TRY(c, launch_series_count(a, c->stream));
+    ++c->series_n;
+    return KMC_OK;
+}
+
 kmc_status exchange_forward(kmc_ctx* c) {
     if (c->world == 1 || c->g.ndim == 1 || !c->comm) return KMC_OK;   // vgroup: exchanged by its driver
     const size_t rowlen = (size_t)c->g.R * c->g.Mx;
@@ -829,7 +851,7 @@ void kmc_destroy(kmc_ctx* c) {
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
     cudaFree(c->flags);
     cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->err_flag);
-    cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv);
+    cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv); cudaFree(c->series);
     cudaFree(c->spare[0]); cudaFree(c->spare[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);
     if (c->h_err) cudaFreeHost(c->h_err);
@@ -988,6 +1010,8 @@ kmc_status kmc_run(kmc_ctx* c, double T, double dt, kmc_scheme scheme) {
             if (st != KMC_OK) return st;
         }
         c->time += d;
+        kmc_status sr = record_sample(c);
+        if (sr != KMC_OK) return sr;
     }
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
@@ -1026,6 +1050,8 @@ kmc_status kmc_run_multiscale(kmc_ctx* c, double T, double dt, int32_t n_fast, k
         if (st == KMC_OK) st = factor(h, slow);
         if (st != KMC_OK) return st;
         c->time += d;
+        kmc_status sr = record_sample(c);
+        if (sr != KMC_OK) return sr;
     }
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
@@ -1053,6 +1079,8 @@ kmc_status kmc_run_nested(kmc_ctx* c, double T, double dt, int32_t n_inner, kmc_
             if (st != KMC_OK) return st;
         }
         c->time += d;
+        kmc_status sr = record_sample(c);
+        if (sr != KMC_OK) return sr;
     }
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
@@ -1225,7 +1253,11 @@ kmc_status kmc_vgroup_run(kmc_ctx** cs, int32_t world, double T, double dt, kmc_
             if (st == KMC_OK && !fused) st = vgroup_reverse(cs, world);
             if (st != KMC_OK) return st;
         }
-        for (int r = 0; r < world; ++r) cs[r]->time += d;
+        for (int r = 0; r < world; ++r) {
+            cs[r]->time += d;
+            kmc_status sr = record_sample(cs[r]);
+            if (sr != KMC_OK) return sr;
+        }
     }
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
@@ -1253,7 +1285,11 @@ kmc_status kmc_vgroup_run_nested(kmc_ctx** cs, int32_t world, double T, double d
             if (st == KMC_OK) st = vgroup_reverse(cs, world);
             if (st != KMC_OK) return st;
         }
-        for (int r = 0; r < world; ++r) cs[r]->time += d;
+        for (int r = 0; r < world; ++r) {
+            cs[r]->time += d;
+            kmc_status sr = record_sample(cs[r]);
+            if (sr != KMC_OK) return sr;
+        }
     }
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
@@ -1345,6 +1381,110 @@ kmc_status kmc_correlation(kmc_ctx* c, int32_t rmax, int32_t state, int64_t* out
         out_x[r] = (int64_t)h[r];
         out_y[r] = (int64_t)h[R1 + r];
     }
+    return KMC_OK;
+}
+
+// ---- f1: the coverage process (R30; Figs. path1D / autocorr1D / pdf2d / dynamics2d) ----
+static long long sites_per_replica(const kmc_ctx* c) {
+    return c->geom.ndim == 1 ? (long long)c->geom.dims[0] : (long long)c->geom.dims[0] * c->geom.dims[1];
+}
+
+kmc_status kmc_record_coverage(kmc_ctx* c, int32_t state, int64_t capacity) {
+    if (!c) return KMC_EINVAL;
+    if (capacity < 0) return fail(c, KMC_EINVAL, "capacity must be >= 0");
+    if (capacity > 0 && (state < 0 || state >= c->nstates)) return fail(c, KMC_EINVAL, "state %d out of range", state);
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));          // no window may still append to the old buffer
+    cudaFree(c->series);
+    c->series = nullptr;
+    c->series_cap = c->series_n = 0;
+    if (capacity == 0) return KMC_OK;
+    if (cudaMalloc((void**)&c->series, (size_t)capacity * c->g.R * 8) != cudaSuccess)
+        return fail(c, KMC_ENOMEM, "coverage series buffer (%lld samples x %d replicas)", (long long)capacity, c->g.R);
+    c->series_cap = capacity;
+    c->series_state = state;
+    return record_sample(c);                                 // sample 0: the current state
+}
+
+// the series with complete per-replica counts: 2D slabs over NCCL ranks hold partial row sums
+static kmc_status full_series(kmc_ctx* c, unsigned long long** out, bool* owned) {
+    *out = c->series;
+    *owned = false;
+    if (c->geom.ndim == 2 && c->world > 1 && c->comm) {
+        const size_t n = (size_t)c->series_n * c->g.R;
+        unsigned long long* t = nullptr;
+        CUDA_TRY(c, cudaMallocAsync((void**)&t, n * 8 + 8, c->stream));
+        NCCL_TRY(c, g_nccl.AllReduce(c->series, t, n, ncclUint64, ncclSum, c->comm, c->stream));
+        *out = t;
+        *owned = true;
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_coverage_series(kmc_ctx* c, int64_t* out, int64_t max_samples, int64_t* n_samples) {
+    if (!c) return KMC_EINVAL;
+    if (n_samples) *n_samples = c->series_n;
+    if (!out || max_samples <= 0 || c->series_n == 0) return KMC_OK;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    unsigned long long* ser = nullptr;
+    bool owned = false;
+    kmc_status st = full_series(c, &ser, &owned);
+    if (st != KMC_OK) return st;
+    const long long n = std::min<long long>(max_samples, c->series_n);
+    CUDA_TRY(c, cudaMemcpyAsync(out, ser, (size_t)n * c->g.R * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (owned) CUDA_TRY(c, cudaFreeAsync(ser, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return KMC_OK;
+}
+
+kmc_status kmc_coverage_stats(kmc_ctx* c, int64_t first, int32_t max_lag, double* acf, double* moments, int32_t bins,
+                              int64_t* hist) {
+    if (!c) return KMC_EINVAL;
+    if (c->vgroup) return fail(c, KMC_ESTATE, "virtual-rank context: counts are per slab (use kmc_coverage_series)");
+    const long long n = c->series_n, nsite = sites_per_replica(c);
+    if (first < 0 || first >= n) return fail(c, KMC_EINVAL, "first %lld outside the %lld recorded samples", (long long)first, n);
+    if (max_lag < 0 || max_lag >= n - first) return fail(c, KMC_EINVAL, "max_lag %d must be < samples - first", max_lag);
+    if (hist && (bins < 1 || bins > nsite + 1 || (double)(nsite + 1) * bins >= 9.2e18))
+        return fail(c, KMC_EINVAL, "bins must be in [1, sites per replica + 1]");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    unsigned long long* ser = nullptr;
+    bool owned = false;
+    kmc_status st = full_series(c, &ser, &owned);
+    if (st != KMC_OK) return st;
+    const bool split = c->geom.ndim == 1 && c->world > 1 && c->comm;   // 1D: replicas sharded over ranks
+    const long long M = split ? (long long)c->geom.replicas : (long long)c->g.R;
+    const long long np = n - first;
+    unsigned long long* d = nullptr;                         // [1 total][max_lag+1 acov][bins hist]
+    const size_t nb = (size_t)(hist ? bins : 0);
+    CUDA_TRY(c, cudaMallocAsync((void**)&d, (size_t)(2 + max_lag + nb) * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(d, 0, (size_t)(2 + max_lag + nb) * 8, c->stream));
+    CUDA_TRY(c, launch_series_total(ser, first, n, c->g.R, d, c->stream));
+    if (split) NCCL_TRY(c, g_nccl.AllReduce(d, d, 1, ncclUint64, ncclSum, c->comm, c->stream));
+    unsigned long long tot = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&tot, d, 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const double mean = (double)tot / ((double)nsite * (double)np * (double)M);
+    double* dacov = reinterpret_cast<double*>(d + 1);
+    unsigned long long* dhist = d + 2 + max_lag;
+    CUDA_TRY(c, launch_series_acov(ser, first, n, c->g.R, max_lag, (double)nsite, mean, dacov, c->stream));
+    if (split) NCCL_TRY(c, g_nccl.AllReduce(dacov, dacov, (size_t)max_lag + 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    if (hist) {
+        CUDA_TRY(c, launch_series_hist(ser, first, n, c->g.R, nsite, bins, dhist, c->stream));
+        if (split) NCCL_TRY(c, g_nccl.AllReduce(dhist, dhist, nb, ncclUint64, ncclSum, c->comm, c->stream));
+    }
+    std::vector<double> hacov((size_t)max_lag + 1);
+    CUDA_TRY(c, cudaMemcpyAsync(hacov.data(), dacov, hacov.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (hist) CUDA_TRY(c, cudaMemcpyAsync(hist, dhist, nb * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaFreeAsync(d, c->stream));
+    if (owned) CUDA_TRY(c, cudaFreeAsync(ser, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const double g0 = hacov[0] / ((double)np * (double)M);
+    if (moments) { moments[0] = mean; moments[1] = g0; }
+    if (acf)
+        for (int l = 0; l <= max_lag; ++l) {
+            const double gl = hacov[(size_t)l] / ((double)(np - l) * (double)M);
+            acf[l] = g0 > 0.0 ? gl / g0 : 0.0;
+        }
     return KMC_OK;
 }
 

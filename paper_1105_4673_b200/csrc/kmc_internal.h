@@ -88,6 +88,27 @@ struct CorrArgs {
 constexpr int kMaxCorrR = 1024;      // largest rmax of kmc_correlation
 cudaError_t launch_correlation(const CorrArgs& a, cudaStream_t s);
 
+// f1: coverage process (R30).  One sample = per-replica count of `state` sites over the owned cells.
+struct SeriesArgs {
+    Geo g;
+    const uint64_t* plane0;
+    const uint64_t* plane1;
+    int nplanes, state;
+    unsigned long long* out;         // [R local] counts of this sample (zeroed by the caller)
+};
+cudaError_t launch_series_count(const SeriesArgs& a, cudaStream_t s);
+// statistics over samples [first, n) of a series [n][R] (counts; coverage = count / nsite_rep):
+//   tot            <- sum of the counts (u64, exact)
+//   acov[l], l = 0..L  <- sum over (i, r), first <= i < n - l, of (c_i - mean)(c_{i+l} - mean), c in coverage
+//                     units (count / nsite_rep); one block per lag, fixed reduction order (deterministic)
+//   hist[b]        <- number of (i, r) with floor(count * bins / (nsite_rep + 1)) = b
+cudaError_t launch_series_total(const unsigned long long* series, long long first, long long n, int R,
+                                unsigned long long* tot, cudaStream_t s);
+cudaError_t launch_series_acov(const unsigned long long* series, long long first, long long n, int R, int L,
+                               double nsite_rep, double mean, double* acov, cudaStream_t s);
+cudaError_t launch_series_hist(const unsigned long long* series, long long first, long long n, int R,
+                               long long nsite_rep, int bins, unsigned long long* hist, cudaStream_t s);
+
 // kernels.cu
 cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cudaStream_t s);
 cudaError_t launch_substep_tile(const SubstepArgs& a, cudaStream_t s);   // kmc_tile.cu (2D spin flip)

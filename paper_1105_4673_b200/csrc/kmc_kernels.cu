@@ -538,6 +538,130 @@ cudaError_t launch_correlation(const CorrArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// f1: the coverage process C_t (Figs. path1D, autocorr1D, pdf2d, dynamics2d; P:1057-1062,
+// P:1121-1127), recorded on the device at macro-step boundaries without a host round trip.
+// series_count_kernel: per-replica number of `state` sites.  Cells are numbered [cy][r][cx], so a
+// warp's lanes mostly share a replica: lanes are grouped by replica (match.any), each group
+// reduced (redux.sync) and its leader does one u64 atomic.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) series_count_kernel(const SeriesArgs a) {
+    const Geo& g = a.g;
+    const uint32_t rowlen = (uint32_t)g.R * g.Mx;
+    const uint32_t ncell = (uint32_t)g.My_local * rowlen;
+    const double inv_mx = 1.0 / (double)g.Mx, inv_r = 1.0 / (double)g.R;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    // warp-uniform trip count (the group reductions need every lane of the warp)
+    for (uint32_t base = blockIdx.x * blockDim.x; base < ncell; base += stride) {
+        const uint32_t t = base + threadIdx.x;
+        const bool ok = t < ncell;
+        uint32_t rest = 0, cx = 0, cy = 0, r = 0;
+        uint32_t cnt = 0;
+        if (ok) {
+            fast_divmod(t, (uint32_t)g.Mx, inv_mx, rest, cx);
+            fast_divmod(rest, (uint32_t)g.R, inv_r, cy, r);
+            const size_t idx = (size_t)(cy + (uint32_t)g.ghost) * rowlen + (size_t)r * g.Mx + cx;
+            const uint64_t p0 = a.plane0[idx];
+            const uint64_t p1 = a.nplanes > 1 ? a.plane1[idx] : 0ull;
+            const uint64_t board = a.state == 1 ? p0 : a.state == 2 ? p1 : (g.valid & ~(p0 | p1));
+            cnt = (uint32_t)__popcll(board);
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, ok ? r : 0xffffffffu);
+        const uint32_t sum = __reduce_add_sync(grp, cnt);
+        if (ok && (threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1) && sum)
+            atomicAdd(&a.out[r], (unsigned long long)sum);
+    }
+}
+
+cudaError_t launch_series_count(const SeriesArgs& a, cudaStream_t s) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long ncell = (long long)a.g.My_local * a.g.R * a.g.Mx;
+    long long nb = (ncell + 255) / 256;
+    if (nb > 8LL * nsm) nb = 8LL * nsm;
+    if (nb < 1) nb = 1;
+    series_count_kernel<<<(unsigned)nb, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// sum of the counts of samples [first, n): one block, exact integer sum
+__global__ void __launch_bounds__(256) series_total_kernel(const unsigned long long* __restrict__ ser, long long first,
+                                                           long long n, int R, unsigned long long* tot) {
+    __shared__ unsigned long long sh[8];
+    unsigned long long acc = 0;
+    const long long lo = first * R, hi = n * R;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += ser[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        *tot = t;
+    }
+}
+
+// acov[l] = sum_{r} sum_{i=first}^{n-1-l} (c_{i,r} - mean)(c_{i+l,r} - mean), c = count / nsite: one
+// block per lag; each thread strides a fixed set of (i, r) pairs and the block tree-reduces in a
+// fixed order, so the result is deterministic.
+__global__ void __launch_bounds__(256) series_acov_kernel(const unsigned long long* __restrict__ ser, long long first,
+                                                          long long n, int R, double nsite, double mean,
+                                                          double* acov) {
+    __shared__ double sh[256];
+    const long long l = blockIdx.x;
+    const long long m = (n - l - first) * R;            // pairs (i, r) with first <= i < n - l
+    double acc = 0.0;
+    for (long long j = threadIdx.x; j < m; j += blockDim.x) {
+        const long long i0 = first * R + j;              // sample i = first + j / R, replica j % R
+        const double a = (double)ser[i0] / nsite - mean;
+        const double b = (double)ser[i0 + l * R] / nsite - mean;
+        acc = __fma_rn(a, b, acc);
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x >> 1; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) acov[l] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) series_hist_kernel(const unsigned long long* __restrict__ ser, long long first,
+                                                          long long n, int R, long long nsite, int bins,
+                                                          unsigned long long* hist) {
+    const long long lo = first * R, hi = n * R;
+    for (long long i = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long c = ser[i];
+        const long long b = (long long)(c * (unsigned long long)bins / (unsigned long long)(nsite + 1));
+        atomicAdd(&hist[b < bins ? b : bins - 1], 1ull);
+    }
+}
+
+cudaError_t launch_series_total(const unsigned long long* ser, long long first, long long n, int R,
+                                unsigned long long* tot, cudaStream_t s) {
+    series_total_kernel<<<1, 256, 0, s>>>(ser, first, n, R, tot);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_series_acov(const unsigned long long* ser, long long first, long long n, int R, int L,
+                               double nsite, double mean, double* acov, cudaStream_t s) {
+    series_acov_kernel<<<(unsigned)(L + 1), 256, 0, s>>>(ser, first, n, R, nsite, mean, acov);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_series_hist(const unsigned long long* ser, long long first, long long n, int R, long long nsite,
+                               int bins, unsigned long long* hist, cudaStream_t s) {
+    const long long m = (n - first) * R;
+    long long nb = (m + 255) / 256;
+    if (nb > 1024) nb = 1024;
+    if (nb < 1) nb = 1;
+    series_hist_kernel<<<(unsigned)nb, 256, 0, s>>>(ser, first, n, R, nsite, bins, hist);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
