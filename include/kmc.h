@@ -140,6 +140,19 @@ kmc_status kmc_get_config_device(kmc_ctx* ctx, uint8_t* dev_local_slab, int64_t 
  * q_x*q_y sites of a cell, or a site both CO and O, give KMC_EINVAL and leave the lattice unchanged.
  * Synchronous. */
 kmc_status kmc_set_config_packed(kmc_ctx* ctx, const uint64_t* host_words, int64_t nwords);
+/* Pipelined upload of the next configuration (same packed layout and validation as
+ * kmc_set_config_packed).  kmc_stage_config_packed enqueues the host->device copy into the
+ * context's spare planes and the validation kernel on a separate copy stream and returns at once,
+ * so the copy overlaps the windows already enqueued (the state they evolve is untouched);
+ * kmc_commit_config then makes the staged configuration current, stream-ordered: windows enqueued
+ * before the commit see the old lattice, windows after it the new one.  The host buffer must stay
+ * valid and unchanged until kmc_commit_config returns (pinned memory gives a truly asynchronous
+ * copy).  One stage may be pending: a second stage, kmc_set_config* while staged, or a commit
+ * without a stage give KMC_ESTATE; a staged configuration that fails validation is discarded by
+ * the commit with KMC_EINVAL (the current lattice is unchanged).  The commit waits (host) for the
+ * staged copy and check only. */
+kmc_status kmc_stage_config_packed(kmc_ctx* ctx, const uint64_t* host_words, int64_t nwords);
+kmc_status kmc_commit_config(kmc_ctx* ctx);
 kmc_status kmc_get_config_packed(kmc_ctx* ctx, uint64_t* host_words, int64_t nwords);
 
 /* Advance physical time by T with macro-steps of dt (R20: n = ceil(T/dt - 1e-9) macro-steps, the

@@ -33,6 +33,7 @@ EXPORTS = [
     "kmc_vgroup_run_nested", "kmc_set_config_packed", "kmc_get_config_packed",
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
     "kmc_vgroup_set_fused", "kmc_abi_sizes", "kmc_record_coverage", "kmc_coverage_series", "kmc_coverage_stats",
+    "kmc_stage_config_packed", "kmc_commit_config",
 ]
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
@@ -118,6 +119,8 @@ def lib():
         "kmc_vgroup_set_fused": ([vp, i32, i32], i32),
         "kmc_abi_sizes": ([vp], None),
         "kmc_record_coverage": ([vp, i32, i64], i32),
+        "kmc_stage_config_packed": ([vp, vp, i64], i32),
+        "kmc_commit_config": ([vp], i32),
         "kmc_coverage_series": ([vp, vp, i64, P(i64)], i32),
         "kmc_coverage_stats": ([vp, i64, i32, vp, vp, i32, vp], i32),
     }
@@ -246,6 +249,22 @@ class KMC:
         if a.size != int(np.prod(self.packed_shape)):
             raise ValueError(f"expected {int(np.prod(self.packed_shape))} words, got {a.size}")
         self._check(self._L.kmc_set_config_packed(self._ctx, a.ctypes.data, a.size))
+
+    def stage_config_packed(self, words):
+        """Pipelined upload (kmc_stage_config_packed): the copy of `words` (packed_shape uint64; pin
+        it for a truly asynchronous copy) overlaps the windows in flight; commit_config() makes it
+        current.  The array is kept referenced until the commit."""
+        a = np.ascontiguousarray(words, dtype=np.uint64)
+        if a.size != int(np.prod(self.packed_shape)):
+            raise ValueError(f"expected {int(np.prod(self.packed_shape))} words, got {a.size}")
+        self._check(self._L.kmc_stage_config_packed(self._ctx, a.ctypes.data, a.size))
+        self._staged_host = a
+
+    def commit_config(self):
+        try:
+            self._check(self._L.kmc_commit_config(self._ctx))
+        finally:
+            self._staged_host = None
 
     def get_config_packed(self):
         out = np.empty(self.packed_shape, dtype=np.uint64)

@@ -137,6 +137,14 @@ struct kmc_ctx {
     unsigned long long* h_obs = nullptr;     // pinned
     unsigned int* h_err = nullptr;           // pinned (set_config validation flag)
     uint64_t* spare[2] = {nullptr, nullptr}; // set_config double buffer
+    // pipelined upload (kmc_stage_config_packed / kmc_commit_config): H2D + validation of the next
+    // configuration into the spare planes on a copy stream, overlapping the windows in flight
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t staged_ev = nullptr;         // copy + check of the staged configuration done
+    cudaEvent_t consumed_ev = nullptr;       // every window that read the current spare has been enqueued before it
+    bool staged = false, consumed_valid = false;
+    unsigned int* stage_err = nullptr;       // device flag of the staged check
+    unsigned int* h_stage_err = nullptr;     // pinned
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
@@ -846,6 +854,11 @@ void kmc_destroy(kmc_ctx* c) {
     // completion signals before the buffers go away
     if (c->fused_ipc && c->flags && c->stream) launch_wait_flags(c->flags, c->epoch, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) { cudaStreamSynchronize(c->copy_stream); cudaStreamDestroy(c->copy_stream); }
+    if (c->staged_ev) cudaEventDestroy(c->staged_ev);
+    if (c->consumed_ev) cudaEventDestroy(c->consumed_ev);
+    cudaFree(c->stage_err);
+    if (c->h_stage_err) cudaFreeHost(c->h_stage_err);
     for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
@@ -897,6 +910,7 @@ static kmc_status ensure_staging(kmc_ctx* c) {
 }
 
 kmc_status kmc_set_config_device(kmc_ctx* c, const uint8_t* dev, int64_t nbytes) {
+    if (c && c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
     if (!c || !dev) return fail(c, KMC_EINVAL, "NULL argument");
     if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
     CUDA_TRY(c, cudaSetDevice(c->device));
@@ -913,6 +927,7 @@ kmc_status kmc_get_config_device(kmc_ctx* c, uint8_t* dev, int64_t nbytes) {
 }
 
 kmc_status kmc_set_config(kmc_ctx* c, const uint8_t* host, int64_t nbytes) {
+    if (c && c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
     if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
     if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
     kmc_status st = ensure_staging(c);
@@ -952,6 +967,7 @@ kmc_status kmc_get_config(kmc_ctx* c, uint8_t* host, int64_t nbytes) {
 static long long packed_words(const kmc_ctx* c) { return (long long)c->nplanes * c->g.My_local * c->g.R * c->g.Mx; }
 
 kmc_status kmc_set_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nwords) {
+    if (c && c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
     if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
     if (nwords != packed_words(c)) return fail(c, KMC_EINVAL, "nwords %lld != packed local slab %lld", (long long)nwords, packed_words(c));
     CUDA_TRY(c, cudaSetDevice(c->device));
@@ -972,6 +988,61 @@ kmc_status kmc_set_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nword
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (*c->h_err) return fail(c, KMC_EINVAL, "packed configuration has bits outside the cells or a site both CO and O");
     return swap_in_spare(c);
+}
+
+kmc_status kmc_stage_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nwords) {
+    if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nwords != packed_words(c)) return fail(c, KMC_EINVAL, "nwords %lld != packed local slab %lld", (long long)nwords, packed_words(c));
+    if (c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (!c->copy_stream) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->staged_ev, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->consumed_ev, cudaEventDisableTiming));
+        if (cudaMalloc((void**)&c->stage_err, 4) != cudaSuccess || cudaMallocHost((void**)&c->h_stage_err, 4) != cudaSuccess)
+            return fail(c, KMC_ENOMEM, "staging flag allocation failed");
+    }
+    for (int p = 0; p < c->nplanes; ++p)
+        if (!c->spare[p] && cudaMalloc((void**)&c->spare[p], (size_t)c->plane_words * 8) != cudaSuccess)
+            return fail(c, KMC_ENOMEM, "spare plane allocation failed");
+    const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
+    const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
+    cudaStream_t cs = c->copy_stream;
+    // the spare planes were the current planes before the last commit: the windows enqueued before
+    // it may still read them
+    if (c->consumed_valid) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->consumed_ev, 0));
+    CUDA_TRY(c, cudaMemsetAsync(c->stage_err, 0, 4, cs));
+    for (int p = 0; p < c->nplanes; ++p)
+        CUDA_TRY(c, cudaMemcpyAsync(c->spare[p] + off, host + (size_t)p * owned, owned * 8, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(c, launch_check_packed(c->spare[0] + off, c->nplanes > 1 ? c->spare[1] + off : nullptr, (long long)owned,
+                                    c->g.valid, c->stage_err, cs));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_stage_err, c->stage_err, 4, cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(c, cudaEventRecord(c->staged_ev, cs));
+    c->staged = true;
+    return KMC_OK;
+}
+
+kmc_status kmc_commit_config(kmc_ctx* c) {
+    if (!c) return KMC_EINVAL;
+    if (!c->staged) return fail(c, KMC_ESTATE, "no staged configuration (kmc_stage_config_packed first)");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaEventSynchronize(c->staged_ev));         // normally long done: it overlapped the windows
+    c->staged = false;
+    if (*c->h_stage_err)
+        return fail(c, KMC_EINVAL, "staged packed configuration has bits outside the cells or a site both CO and O (discarded)");
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->staged_ev, 0));
+    if (c->g.ghost) {   // ghost rows are refreshed by the next exchange; keep them defined (stream-ordered)
+        const size_t row = (size_t)c->g.R * c->g.Mx, last = (size_t)(c->g.My_local + 1) * row;
+        for (int p = 0; p < c->nplanes; ++p) {
+            CUDA_TRY(c, cudaMemcpyAsync(c->spare[p], c->planes[p], row * 8, cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_TRY(c, cudaMemcpyAsync(c->spare[p] + last, c->planes[p] + last, row * 8, cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
+    kmc_status st = swap_in_spare(c);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->consumed_ev, c->stream));
+    c->consumed_valid = true;
+    return KMC_OK;
 }
 
 kmc_status kmc_get_config_packed(kmc_ctx* c, uint64_t* host, int64_t nwords) {

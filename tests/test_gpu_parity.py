@@ -450,6 +450,62 @@ def test_packed_config_validation():
         g.set_config_packed(w[:, :1])
 
 
+@pytest.mark.parametrize("kind,dims,cell,params", [
+    ("adsdes", (64, 64), (8, 8), dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)),
+    ("zgb", (32, 32), (4, 4), dict(k1=0.4, k2=1.0)),
+])
+def test_staged_config_pipelined_upload(kind, dims, cell, params):
+    """kmc_stage_config_packed / kmc_commit_config: the staged copy overlaps the run in flight
+    without touching it; after the commit the next run starts from the staged lattice, bit-identical
+    to the synchronous set_config_packed path; protocol errors are KMC_ESTATE and an invalid staged
+    configuration is discarded at the commit (KMC_EINVAL, lattice unchanged)."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    a = kmc.KMC(2, dims, cell, kind=kind, replicas=2, seed=9, **params)
+    b = kmc.KMC(2, dims, cell, kind=kind, replicas=2, seed=9, **params)
+    np_ = a.packed_shape[0]
+    mk = ((lambda s: si.bernoulli_lattice(a.local_shape, 0.5, seed=s)) if kind == "adsdes"
+          else (lambda s: si.categorical_lattice(a.local_shape, [0.5, 0.25, 0.25], seed=s)))
+    lat1, lat2 = mk(1), mk(2)
+    w1, w2 = _pack_words(lat1, *cell, np_), _pack_words(lat2, *cell, np_)
+    a.set_config_packed(w1)
+    b.set_config_packed(w1)
+    for step in range(3):
+        a.run(2.0, 0.5, "strang")                      # enqueued, may still be running ...
+        a.stage_config_packed(w2 if step % 2 == 0 else w1)   # ... while the next input is copied
+        b.run(2.0, 0.5, "strang")
+        assert np.array_equal(a.get_config(), b.get_config()), "staging touched the running state"
+        a.commit_config()
+        b.set_config_packed(w2 if step % 2 == 0 else w1)
+        assert np.array_equal(a.get_config(), b.get_config())
+    a.run(1.0, 0.5, "lie")
+    b.run(1.0, 0.5, "lie")
+    assert np.array_equal(a.get_config(), b.get_config())
+    assert a.observables()["events"] == b.observables()["events"]
+    with pytest.raises(kmc.KmcError) as e:
+        a.commit_config()                              # nothing staged
+    assert e.value.status == 6
+    a.stage_config_packed(w2)
+    with pytest.raises(kmc.KmcError):
+        a.stage_config_packed(w2)                      # one pending stage at a time
+    with pytest.raises(kmc.KmcError):
+        a.set_config(lat1)                             # synchronous setters wait for the commit
+    a.commit_config()
+    assert np.array_equal(a.get_config(), lat2)
+    if kind == "zgb":
+        bad = w1.copy()
+        bad[1, 1, 0, 1] |= bad[0, 1, 0, 1] | np.uint64(1)    # a site both CO and O
+        bad[0, 1, 0, 1] |= np.uint64(1)
+        a.stage_config_packed(bad)
+        with pytest.raises(kmc.KmcError) as e:
+            a.commit_config()
+        assert e.value.status == 1
+        assert np.array_equal(a.get_config(), lat2)
+        a.stage_config_packed(w1)                      # usable again after the rejected commit
+        a.commit_config()
+        assert np.array_equal(a.get_config(), lat1)
+
+
 def _half_full(shape):
     lat = np.zeros(shape, dtype=np.uint8)
     lat[:, : shape[1] // 2] = 1                 # top half full: few events; bottom half empty: many
