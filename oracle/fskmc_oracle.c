@@ -141,9 +141,10 @@ int orc_classes(int kind, int ndim, const double* params,
             ctype[n] = T_DES; cdir[n] = -1; ckappa[n] = m; crate[n] = cd * exp(t); ++n;
         }
         if (kind == M_ADSDES_DIFF) {
-            /* R12: hop x->y (y vacant) at c_hop exp(-beta K n(x)) */
-            for (int d = 0; d < z; ++d)
-                for (int m = 0; m <= z - 1; ++m) {
+            /* R12: hop x->y (y vacant) at c_hop exp(-beta K n(x)); R31: classes n-major
+             * (n(x) = 0..z-1 outer, direction d inner) */
+            for (int m = 0; m <= z - 1; ++m)
+                for (int d = 0; d < z; ++d) {
                     double t = K * (double)m;
                     t = beta * t;
                     t = -t;

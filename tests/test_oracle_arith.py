@@ -67,10 +67,13 @@ def test_rate_table_quantisation_R18():
     assert bound * 2.0 ** F <= 2.0 ** 62 < 2 * bound * 2.0 ** F
     for r, u in zip(t["rate"], t["rate_u64"]):
         assert abs(int(u) - r * 2.0 ** F) <= 0.5
-    # hops: c_hop exp(-beta K n), n = 0..z-1, per direction (R12)
+    # hops: c_hop exp(-beta K n), n = 0..z-1, per direction (R12), n-major (R31)
     assert t["n"] == 6 + 16
     assert list(t["type"][6:]) == [2] * 16
-    assert list(t["dir"][6:]) == [d for d in range(4) for _ in range(4)]
+    assert list(t["dir"][6:]) == [d for _ in range(4) for d in range(4)]
+    assert list(t["kappa"][6:]) == [n for n in range(4) for _ in range(4)]
+    for i in range(6, 22):
+        assert math.isclose(t["rate"][i], math.exp(-1.5 * t["kappa"][i]), rel_tol=1e-15)
 
 
 def test_rate_table_zgb_table_COrates():
