@@ -207,8 +207,8 @@ int build_classes(const kmc_model& m, int ndim, int* type, int* dir, int* kappa,
             add(T_DES, -1, nn, m.cd * std::exp(u));
         }
         if (m.kind == KMC_ADSDES_DIFF)
-            for (int d = 0; d < z; ++d)
-                for (int nn = 0; nn < z; ++nn) {                   // R12: c_hop exp(-beta K n(x))
+            for (int nn = 0; nn < z; ++nn)                         // R31: n-major, direction inner
+                for (int d = 0; d < z; ++d) {                      // R12: c_hop exp(-beta K n(x))
                     double u = m.K * (double)nn;
                     u = m.beta * u;
                     u = -u;
@@ -416,6 +416,17 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
     if (class_mask != ~0ull)
         for (int i = 0; i < c->nclass; ++i) a.rate[i] = ((class_mask >> i) & 1ull) ? c->crate_u64[i] : 0ull;
+    if (c->kind == KMC_ADSDES_DIFF) {   // R31 hop blocks: one rate per block -> the block-walk kernel
+        const int z = 2 * c->g.ndim;
+        a.hop_fast = 1;
+        for (int n = 0; n < z; ++n) {
+            const uint64_t r = a.rate[2 + z + n * z];
+            for (int d = 1; d < z; ++d) a.hop_fast &= a.rate[2 + z + n * z + d] == r ? 1 : 0;
+            a.hopz[n] = (uint64_t)(z - n) * r;
+        }
+        static const int hop_env = [] { const char* e = getenv("KMC_HOPFAST"); return e ? atoi(e) : 1; }();
+        if (!hop_env) a.hop_fast = 0;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         if (c->tev_used == c->tev.size()) {

@@ -252,7 +252,9 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     bool pend = false;
     const uint32_t refill_min = (uint32_t)a.refill_min;
     for (;;) {
-        const bool fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
+        bool fin;
+        if constexpr (KIND == 4) fin = event_step_hop<NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
+        else fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
         pend = pend || fin;
         have = have && !fin;
         const unsigned fm = __ballot_sync(FULL, pend);
@@ -345,6 +347,21 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
         // (22 masks live) is fastest with <= 128 registers (2 CTAs/SM), ZGB (counts + rebuilt mask)
         // with <= 80 registers (3 CTAs/SM) -- measured on B200
         if (!mh_ok) return cudaErrorInvalidValue;
+        if constexpr (KIND == 1) {
+            // uniform hop blocks (R31): the block-walk step (8192^2 Strang: 2.93e10 events/s vs 2.29e10
+            // for the 22-mask step), 101 registers (2 CTAs/SM; the <= 80-register build, KMC_HOPLB=3,
+            // measured 2 % slower)
+            static const int hlb = [] { const char* e = getenv("KMC_HOPLB"); return e ? atoi(e) : 2; }();
+            if (a.hop_fast) {
+                if (a.nest) return hlb == 2 ? launch_v<4, NDIM, 2, true, true>(a, nactive, s)
+                                            : launch_v<4, NDIM, 3, true, true>(a, nactive, s);
+                if (NDIM == 2 && a.peer_up[0])
+                    return hlb == 2 ? launch_v<4, NDIM, 2, true, false, NDIM == 2>(a, nactive, s)
+                                    : launch_v<4, NDIM, 3, true, false, NDIM == 2>(a, nactive, s);
+                return hlb == 2 ? launch_v<4, NDIM, 2, true, false>(a, nactive, s)
+                                : launch_v<4, NDIM, 3, true, false>(a, nactive, s);
+            }
+        }
         const bool big = (KIND == 1 && lb != 4) || lb == 3;
         if (a.nest) return big ? launch_v<KIND, NDIM, 2, true, true>(a, nactive, s)
                                : launch_v<KIND, NDIM, 3, true, true>(a, nactive, s);
