@@ -359,6 +359,7 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
                     return hlb == 2 ? launch_v<4, NDIM, 2, true, false, NDIM == 2>(a, nactive, s)
                                     : launch_v<4, NDIM, 3, true, false, NDIM == 2>(a, nactive, s);
                 return hlb == 2 ? launch_v<4, NDIM, 2, true, false>(a, nactive, s)
+                     : hlb == 4 ? launch_v<4, NDIM, 4, true, false>(a, nactive, s)
                                 : launch_v<4, NDIM, 3, true, false>(a, nactive, s);
             }
         }
@@ -439,11 +440,17 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
             acc[s] += c;
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) acc[4 + cc * 4 + s] += colour == cc ? c : 0u;
+            // bonds (x, x+e) by the neighbour's state b: the boards B[b] partition the sites, so the
+            // last state's count is the site count minus the others (one popc pair fewer per s)
+            uint32_t rest = NDIM == 2 ? 2 * c : c;
 #pragma unroll
-            for (int b = 0; b < NS; ++b) {
-                acc[20 + s * 4 + b] += __popcll(A[s] & Bx[b]);
-                if (NDIM == 2) acc[20 + s * 4 + b] += __popcll(A[s] & By[b]);
+            for (int b = 0; b + 1 < NS; ++b) {
+                uint32_t v = __popcll(A[s] & Bx[b]);
+                if (NDIM == 2) v += __popcll(A[s] & By[b]);
+                acc[20 + s * 4 + b] += v;
+                rest -= v;
             }
+            acc[20 + s * 4 + NS - 1] += rest;
         }
     }
 #pragma unroll

@@ -316,6 +316,26 @@ def test_multiscale_bit_exact(ndim, dims, cell, kind, params, inner, nf):
     assert orc.events > 0
 
 
+@pytest.mark.parametrize("ndim,dims,cell", [(2, (64, 64), (4, 4)), (1, (256,), (8,))])
+def test_multiscale_split_hop_blocks_bit_exact(ndim, dims, cell):
+    """f2 with a fast set that splits the R31 hop blocks (x-direction hops fast, y-direction hops and
+    the spin flips slow): hop rates differ within a block, so the windows run the generic 22-mask
+    diffusion step instead of the block-walk step -- bit-exact vs O2 either way."""
+    z = 2 * ndim
+    fast = [2 + z + n * z + d for n in range(z) for d in (0, 1) if d < z and (ndim == 2 or d == 0)]
+    params = dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=6.0)
+    gpu, orc = make_pair(ndim, dims, cell, "adsdes_diff", params, 0, 2)
+    lat = si.bernoulli_lattice(gpu.local_shape, 0.4, seed=13)
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    mask = sum(1 << c for c in fast)
+    for _ in range(2):
+        gpu.run_multiscale(1.0, 0.5, 3, "strang", fast_classes=mask)
+        orc.run_multiscale(1.0, 0.5, 3, "strang", fast_classes=fast)
+        assert_same_state(gpu, orc, "multiscale split hop blocks")
+    assert orc.events > 0
+
+
 NESTED = [
     # ndim, dims, cell, kind, params, block, outer, inner, n_inner
     (2, (64, 128), (8, 8), "adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), 2, "lie", "lie", 2),
