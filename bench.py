@@ -83,18 +83,38 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def oracle_sample(wl, sites):
+    """A bounded sample of the workload for the O2 oracle: a side x side periodic sub-lattice in 2D,
+    in 1D the workload's ring (truncated to `sites`) with as many replicas as fill `sites`."""
+    from oracle.fskmc import FSKMC, model_params
+    if wl["ndim"] == 2:
+        side = int(round(sites ** 0.5))
+        dims, R, desc = (side, side), 1, f"{side}x{side} periodic sub-lattice"
+        shape = (1, side, side)
+    else:
+        N = min(wl["dims"][0], sites)
+        R = max(1, sites // N)
+        dims, desc = (N,), f"{R} x {N}-site rings"
+        shape = (R, 1, N)
+    o = FSKMC(wl["ndim"], dims, wl["cell"], wl["kind"], model_params(**wl["params"]), replicas=R, seed=7)
+    if wl["kind"].startswith("zgb"):
+        lat = si.categorical_lattice(shape, [1.0 - wl["init"], wl["init"] / 2, wl["init"] / 2] if wl["init"]
+                                     else [1.0, 0.0, 0.0], seed=si.SEED_BASE + 1)
+    else:
+        lat = si.bernoulli_lattice(shape, wl["init"], seed=si.SEED_BASE + 1)
+    o.set_config(lat)
+    return o, desc
+
+
 def cpu_baseline_sample(wl, seconds_hint="~10-30 s"):
     """The O2 oracle as it stands, on a bounded sample of the workload (rank 0, N = 1)."""
-    from oracle.fskmc import FSKMC, model_params
-    side = 512
-    o = FSKMC(wl["ndim"], (side, side), wl["cell"], wl["kind"], model_params(**wl["params"]), seed=7)
-    o.set_config(si.bernoulli_lattice((1, side, side), wl["init"], seed=si.SEED_BASE + 1))
+    o, desc = oracle_sample(wl, 512 * 512)
     t0 = time.perf_counter()
     nmacro = 4                                         # ~15 s of single-thread oracle work
     o.run(nmacro * wl["dt"], wl["dt"], wl["scheme"])
     el = time.perf_counter() - t0
     return {"value": o.events / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"O2 oracle, {side}x{side} periodic sub-lattice of the workload, {nmacro} {wl['scheme']} "
+            "sample": f"O2 oracle, {desc} of the workload, {nmacro} {wl['scheme']} "
                       f"macro-steps dt={wl['dt']}, {o.events} events in {el:.1f} s, 1 thread"}
 
 
@@ -110,6 +130,7 @@ def arm_config(workload, dt, world, fused=False, scaling="weak"):
     return {"workload": workload, "dims_per_gpu": per_gpu, "global_dims": global_dims, "cell": list(wl["cell"]),
             "model": wl["kind"], "params": wl["params"], "scheme": wl["scheme"], "dt": dt,
             "init": f"Bernoulli({wl['init']})", "colours": C,
+            "replicas_per_gpu": wl.get("replicas_per_gpu", 1),
             "l2": "inputs larger than L2 (bit-packed lattice 128 MiB/GPU at 32768^2 > 126 MB L2)",
             "parallelism": (f"slab{world}" if wl["ndim"] == 2 else f"replicas{world}"),
             "exchange": ("fused (peer writes in the window kernel)" if fused else "nccl send/recv")
@@ -121,11 +142,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.fskmc import FSKMC, model_params
     wl = si.WORKLOADS[args.workload]
-    side = 256
-    o = FSKMC(wl["ndim"], (side, side), wl["cell"], wl["kind"], model_params(**wl["params"]), seed=7)
-    o.set_config(si.bernoulli_lattice((1, side, side), wl["init"], seed=si.SEED_BASE + 1))
+    o, desc = oracle_sample(wl, 256 * 256)
     dt = args.dt if args.dt is not None else wl["dt"]
     for _ in range(args.warmup):
         o.run(dt, dt, wl["scheme"])
@@ -136,7 +154,7 @@ def run_reference(args):
         o.observables()
     el = time.perf_counter() - t0
     v = (o.events - e0) / el
-    sample = f"O2 oracle on a {side}x{side} periodic sub-lattice of {args.workload}, 1 macro-step per step, 1 thread"
+    sample = f"O2 oracle on {desc} of {args.workload}, 1 macro-step per step, 1 thread"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / max(1, args.steps),
@@ -194,7 +212,7 @@ def main():
     else:
         gdims = wl["dims"]
     stream = torch.cuda.current_stream()
-    k = kmc.KMC(ndim, gdims, wl["cell"], kind=wl["kind"], replicas=wl.get("replicas", world if ndim == 1 else 1),
+    k = kmc.KMC(ndim, gdims, wl["cell"], kind=wl["kind"], replicas=wl.get("replicas_per_gpu", 1) * (world if ndim == 1 else 1),
                 seed=0xB200, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=uid,
                 fused_exchange=args.fused_exchange and world > 1, **wl["params"])
     shape = k.local_shape
@@ -213,7 +231,7 @@ def main():
     host_pk_np = host_pk.numpy().view(np.uint64).reshape(packed.shape)
     del lat, packed
     k.set_config_device(dev.data_ptr(), dev.numel())
-    sites = int(np.prod(gdims)) * (wl.get("replicas", 1))
+    sites = int(np.prod(gdims)) * k.local_shape[0] * (world if ndim == 1 else 1)
     C = 2 if (ndim == 1 or wl["kind"] == "adsdes") else 4
 
     def step():

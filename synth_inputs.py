@@ -80,6 +80,15 @@ WORKLOADS = {
     "ising1d_65536": dict(ndim=1, dims=(65536,), cell=(32,), kind="adsdes",
                           params=dict(ca=1.0, cd=1.0, beta=2.0, K=1.0, h=0.0),
                           scheme="lie", dt=1.0, init=0.0),
+    # cfg2 as SURVEY §8(d) runs it: 64 independent replicas per GPU (the paper averages over
+    # M = 1000 realisations)
+    "ising1d_65536x64": dict(ndim=1, dims=(65536,), cell=(32,), kind="adsdes",
+                             params=dict(ca=1.0, cd=1.0, beta=2.0, K=1.0, h=0.0),
+                             scheme="lie", dt=1.0, init=0.0, replicas_per_gpu=64),
+    # cfg1: non-interacting 1D, N = 1024, Q = 32, M = 1000 replicas per GPU, Lie dt = 0.1
+    "noninteracting1d_1024x1000": dict(ndim=1, dims=(1024,), cell=(32,), kind="adsdes",
+                                       params=dict(ca=1.0, cd=0.5, beta=1.0, K=0.0, h=0.0),
+                                       scheme="lie", dt=0.1, init=0.0, replicas_per_gpu=1000),
     "diff2d_8192": dict(ndim=2, dims=(8192, 8192), cell=(8, 8), kind="adsdes_diff",
                         params=dict(ca=1.0, cd=1.0, beta=1.5, K=1.0, h=-2.0, c_hop=1.0),
                         scheme="strang", dt=1.0, init=0.5),
