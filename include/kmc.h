@@ -194,6 +194,18 @@ kmc_status kmc_substep(kmc_ctx* ctx, int32_t colour, double duration);
  * sums the counters over ranks (NCCL all-reduce). */
 kmc_status kmc_observables(kmc_ctx* ctx, kmc_obs* out, uint32_t* per_cell_events);
 
+/* Device-resident observables (a8 with no host round trip, e.g. once per macro-step inside a timed
+ * or graph-captured loop): kmc_observables_device enqueues the counters of the current state into
+ * dev_counters (KMC_OBS_WORDS uint64 in device memory of the context's device, caller-owned):
+ * [0..3] sites per state, [4..19] sites per state by cell colour [colour*4 + state], [20..35]
+ * ordered nearest-neighbour bonds (x, x+e), e in {+x, +y}, [a*4 + b], [36] events, [37] windows,
+ * [38] time (IEEE double bits), [39] 0.  Stream-ordered, asynchronous; world > 1 sums words 0..36
+ * over the NCCL ranks (collective).  kmc_obs_decode turns a host copy of those words into a kmc_obs
+ * (what kmc_observables returns for the same state). */
+#define KMC_OBS_WORDS 40
+kmc_status kmc_observables_device(kmc_ctx* ctx, uint64_t* dev_counters);
+kmc_status kmc_obs_decode(const kmc_ctx* ctx, const uint64_t* counters, kmc_obs* out);
+
 /* Two-point correlation counts (the paper's 2-point correlation function
  * E[sigma_t(x) sigma_t(x+y)]): out_x[r] (r = 0..rmax) = number of sites x with
  * sigma(x) = state and sigma(x + r e_x) = state, summed over the whole lattice (periodic, all

@@ -33,8 +33,9 @@ EXPORTS = [
     "kmc_vgroup_run_nested", "kmc_set_config_packed", "kmc_get_config_packed",
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
     "kmc_vgroup_set_fused", "kmc_abi_sizes", "kmc_record_coverage", "kmc_coverage_series", "kmc_coverage_stats",
-    "kmc_stage_config_packed", "kmc_commit_config",
+    "kmc_stage_config_packed", "kmc_commit_config", "kmc_observables_device", "kmc_obs_decode",
 ]
+OBS_WORDS = 40
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
 
 
@@ -120,6 +121,8 @@ def lib():
         "kmc_abi_sizes": ([vp], None),
         "kmc_record_coverage": ([vp, i32, i64], i32),
         "kmc_stage_config_packed": ([vp, vp, i64], i32),
+        "kmc_observables_device": ([vp, vp], i32),
+        "kmc_obs_decode": ([vp, vp, P(KmcObs)], i32),
         "kmc_commit_config": ([vp], i32),
         "kmc_coverage_series": ([vp, vp, i64, P(i64)], i32),
         "kmc_coverage_stats": ([vp, i64, i32, vp, vp, i32, vp], i32),
@@ -327,16 +330,34 @@ class KMC:
             cells = np.zeros((R, H // qy, W // qx), dtype=np.uint32)
             ptr = cells.ctypes.data
         self._check(self._L.kmc_observables(self._ctx, ctypes.byref(o), ptr))
-        d = {
+        d = self._obs_dict(o)
+        if per_cell:
+            d["per_cell_events"] = cells
+        return d
+
+    @staticmethod
+    def _obs_dict(o):
+        return {
             "time": o.time, "windows": int(o.windows), "events": int(o.events),
             "n_state": np.array(o.n_state[:], dtype=np.int64),
             "nn_pairs": np.array([o.nn_pairs[i][:] for i in range(4)], dtype=np.int64),
             "n_state_by_colour": np.array([o.n_state_by_colour[i][:] for i in range(4)], dtype=np.int64),
             "coverage": np.array(o.coverage[:]), "energy": o.energy,
         }
-        if per_cell:
-            d["per_cell_events"] = cells
-        return d
+
+    def observables_device(self, dev_ptr):
+        """kmc_observables_device: enqueue the a8 counters of the current state into OBS_WORDS
+        uint64 at device address dev_ptr (e.g. a torch int64 tensor's data_ptr()); no host sync."""
+        self._check(self._L.kmc_observables_device(self._ctx, ctypes.c_void_p(int(dev_ptr))))
+
+    def obs_decode(self, words):
+        """kmc_obs_decode of a host copy of the OBS_WORDS counters: the observables() dict."""
+        a = np.ascontiguousarray(words)
+        if a.dtype != np.uint64:
+            a = a.astype(np.int64).view(np.uint64)
+        o = KmcObs()
+        self._check(self._L.kmc_obs_decode(self._ctx, a.ctypes.data, ctypes.byref(o)))
+        return self._obs_dict(o)
 
     def correlation(self, rmax, state=1):
         """Two-point correlation counts (kmc_correlation): {'x': int64[rmax+1], 'y': int64[rmax+1]},

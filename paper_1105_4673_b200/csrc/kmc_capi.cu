@@ -129,7 +129,7 @@ struct kmc_ctx {
     long long series_cap = 0, series_n = 0;
     int series_state = 1;
     unsigned int* queue = nullptr;           // window kernel's dynamic chunk counter
-    unsigned long long* obs_buf = nullptr;   // kObsCounters + 1 (events)
+    unsigned long long* obs_buf = nullptr;   // KMC_OBS_WORDS (enqueue_obs layout)
     unsigned int* err_flag = nullptr;
     uint8_t* staging = nullptr;              // uint8 local slab (set/get_config from host)
     uint64_t* ghost_snap = nullptr;          // [2 rows][nplanes] snapshot / delta buffers (world > 1)
@@ -821,13 +821,13 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     ok = ok && alloc((void**)&c->wmark, (size_t)owned * 4);
     ok = ok && alloc((void**)&c->ev_total, 8);
     ok = ok && alloc((void**)&c->queue, 8);
-    ok = ok && alloc((void**)&c->obs_buf, (kObsCounters + 1) * 8);
+    ok = ok && alloc((void**)&c->obs_buf, KMC_OBS_WORDS * 8);
     ok = ok && alloc((void**)&c->err_flag, 4);
     if (g.ghost) {
         ok = ok && alloc((void**)&c->ghost_snap, (size_t)4 * g.R * g.Mx * 8);
         ok = ok && alloc((void**)&c->ghost_recv, (size_t)4 * g.R * g.Mx * 8);
     }
-    ok = ok && cudaMallocHost((void**)&c->h_obs, (kObsCounters + 1) * 8) == cudaSuccess;
+    ok = ok && cudaMallocHost((void**)&c->h_obs, KMC_OBS_WORDS * 8) == cudaSuccess;
     ok = ok && cudaMallocHost((void**)&c->h_err, 4) == cudaSuccess;
     if (!ok) { kmc_destroy(c); return fail(nullptr, KMC_ENOMEM, "device allocation failed (%lld words)", c->plane_words); }
     for (int p = 0; p < c->nplanes; ++p) cudaMemsetAsync(c->planes[p], 0, (size_t)c->plane_words * 8, c->stream);
@@ -1376,35 +1376,34 @@ kmc_status kmc_vgroup_run_nested(kmc_ctx** cs, int32_t world, double T, double d
     return truncated ? KMC_WTRUNCATED : KMC_OK;
 }
 
-kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
-    if (!c || !o) return fail(c, KMC_EINVAL, "NULL argument");
-    CUDA_TRY(c, cudaSetDevice(c->device));
+// a8 counters of the current state into out[KMC_OBS_WORDS] (device), stream-ordered: [0..35] the
+// observables kernel's counters, [36] events (all ranks), [37] windows, [38] time (double bits)
+static kmc_status enqueue_obs(kmc_ctx* c, unsigned long long* out) {
     kmc_status st = exchange_forward(c);   // ghosts current for the +y bonds of the last owned row
     if (st != KMC_OK) return st;
-    CUDA_TRY(c, cudaMemsetAsync(c->obs_buf, 0, kObsCounters * 8, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(c->obs_buf + kObsCounters, c->ev_total, 8, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(out, 0, KMC_OBS_WORDS * 8, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(out + kObsCounters, c->ev_total, 8, cudaMemcpyDeviceToDevice, c->stream));
     ObsArgs a{};
     a.g = c->g;
     a.plane0 = c->planes[0];
     a.plane1 = c->planes[1];
     a.nplanes = c->nplanes;
     a.C = c->C;
-    a.out = c->obs_buf;
+    a.out = out;
+    a.windows = c->window;
+    a.time = c->time;
     CUDA_TRY(c, launch_observables(a, c->stream));
     if (c->world > 1 && c->comm)   // NCCL ranks: global sums (virtual ranks return local counts)
-        NCCL_TRY(c, g_nccl.AllReduce(c->obs_buf, c->obs_buf, kObsCounters + 1, ncclUint64, ncclSum, c->comm, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_obs, c->obs_buf, (kObsCounters + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
-    std::vector<uint32_t> wl;
-    const long long owned = (long long)c->g.My_local * c->g.R * c->g.Mx;
-    if (per_cell) {
-        wl.resize((size_t)owned);
-        CUDA_TRY(c, cudaMemcpyAsync(wl.data(), c->wev, (size_t)owned * 4, cudaMemcpyDeviceToHost, c->stream));
-    }
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    const unsigned long long* h = c->h_obs;
+        NCCL_TRY(c, g_nccl.AllReduce(out, out, kObsCounters + 1, ncclUint64, ncclSum, c->comm, c->stream));
+    return KMC_OK;
+}
+
+static void decode_obs(const kmc_ctx* c, const unsigned long long* h, kmc_obs* o) {
     memset(o, 0, sizeof *o);
-    o->time = c->time;
-    o->windows = c->window;
+    double t;
+    memcpy(&t, &h[kObsCounters + 2], 8);
+    o->time = t;
+    o->windows = h[kObsCounters + 1];
     o->events = h[kObsCounters];
     long long total = 0;
     for (int s = 0; s < 4; ++s) { o->n_state[s] = (int64_t)h[s]; total += (long long)h[s]; }
@@ -1418,12 +1417,40 @@ kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
         }
     for (int s = 0; s < 4; ++s) o->coverage[s] = total ? (double)o->n_state[s] / (double)total : 0.0;
     o->energy = -c->model.K * (double)o->nn_pairs[1][1] + c->model.h * (double)o->n_state[1];   // R24
+}
+
+kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
+    if (!c || !o) return fail(c, KMC_EINVAL, "NULL argument");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st = enqueue_obs(c, c->obs_buf);
+    if (st != KMC_OK) return st;
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_obs, c->obs_buf, KMC_OBS_WORDS * 8, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<uint32_t> wl;
+    const long long owned = (long long)c->g.My_local * c->g.R * c->g.Mx;
+    if (per_cell) {
+        wl.resize((size_t)owned);
+        CUDA_TRY(c, cudaMemcpyAsync(wl.data(), c->wev, (size_t)owned * 4, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    decode_obs(c, c->h_obs, o);
     if (per_cell) {   // device order [cy][r][cx] -> [r][cy][cx]
         const int R = c->g.R, My = c->g.My_local, Mx = c->g.Mx;
         for (int cy = 0; cy < My; ++cy)
             for (int r = 0; r < R; ++r)
                 memcpy(per_cell + ((size_t)r * My + cy) * Mx, wl.data() + ((size_t)cy * R + r) * Mx, (size_t)Mx * 4);
     }
+    return KMC_OK;
+}
+
+kmc_status kmc_observables_device(kmc_ctx* c, uint64_t* dev_counters) {
+    if (!c || !dev_counters) return fail(c, KMC_EINVAL, "NULL argument");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return enqueue_obs(c, reinterpret_cast<unsigned long long*>(dev_counters));
+}
+
+kmc_status kmc_obs_decode(const kmc_ctx* c, const uint64_t* counters, kmc_obs* out) {
+    if (!c || !counters || !out) return KMC_EINVAL;
+    decode_obs(c, reinterpret_cast<const unsigned long long*>(counters), out);
     return KMC_OK;
 }
 

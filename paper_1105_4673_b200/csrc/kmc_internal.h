@@ -75,7 +75,9 @@ struct ObsArgs {
     const uint64_t* plane0;
     const uint64_t* plane1;
     int nplanes, C;
-    unsigned long long* out;         // [4 n_state][16 by_colour][16 nn ordered]
+    unsigned long long* out;         // [4 n_state][16 by_colour][16 nn ordered], then events, windows, time
+    unsigned long long windows;      // written to out[37] / out[38] by one thread (host values at enqueue)
+    double time;
 };
 
 constexpr int kObsCounters = 4 + 16 + 16;

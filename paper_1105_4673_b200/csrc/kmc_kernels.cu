@@ -397,6 +397,10 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
     const Geo& g = a.g;
     __shared__ unsigned long long sh[kObsCounters];
     for (int i = threadIdx.x; i < kObsCounters; i += blockDim.x) sh[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.out[kObsCounters + 1] = a.windows;
+        a.out[kObsCounters + 2] = (unsigned long long)__double_as_longlong(a.time);
+    }
     __syncthreads();
     uint32_t acc[kObsCounters];
 #pragma unroll

@@ -142,6 +142,33 @@ def test_observables_match_oracle():
         assert abs(a["energy"] - b["energy"]) <= 1e-9 * max(1.0, abs(b["energy"]))
 
 
+@pytest.mark.parametrize("kind,ndim,dims,cell", [("adsdes", 2, (64, 64), (8, 8)), ("zgb", 2, (32, 32), (4, 4)),
+                                                  ("adsdes_diff", 1, (256,), (8,))])
+def test_observables_device_matches_sync(kind, ndim, dims, cell):
+    """kmc_observables_device (enqueued, no host sync) + kmc_obs_decode == kmc_observables for the
+    same states, including the events, windows and time words; several snapshots in one buffer."""
+    torch = _cuda()
+    import paper_1105_4673_b200 as kmc
+    g = kmc.KMC(ndim, dims, cell, kind=kind, replicas=2, seed=4)
+    lat = (si.bernoulli_lattice(g.local_shape, 0.5, seed=3) if g.nstates == 2
+           else si.categorical_lattice(g.local_shape, [0.5, 0.25, 0.25], seed=3))
+    g.set_config(lat)
+    buf = torch.zeros((4, kmc.OBS_WORDS), dtype=torch.int64, device="cuda")
+    ref = []
+    for i in range(4):
+        g.run(0.5, 0.25, "strang")
+        g.observables_device(buf[i].data_ptr())
+        ref.append(g.observables())
+    host = buf.cpu().numpy()
+    for i in range(4):
+        got = g.obs_decode(host[i])
+        for key in ("time", "windows", "events", "energy"):
+            assert got[key] == ref[i][key], (i, key)
+        for key in ("n_state", "nn_pairs", "n_state_by_colour", "coverage"):
+            assert np.array_equal(got[key], ref[i][key]), (i, key)
+    assert host[3, 37] == ref[3]["windows"] and host[3, 39] == 0
+
+
 def test_resume_run_split_equals_whole():
     p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0, c_hop=1.0)
     import paper_1105_4673_b200 as kmc
