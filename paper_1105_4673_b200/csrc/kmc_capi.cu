@@ -130,6 +130,7 @@ struct kmc_ctx {
     int series_state = 1;
     unsigned int* queue = nullptr;           // window kernel's dynamic chunk counter
     unsigned long long* obs_buf = nullptr;   // KMC_OBS_WORDS (enqueue_obs layout)
+    unsigned long long* obs_acc = nullptr;   // kObsCounters + 1: the observables kernel's accumulator + ticket
     unsigned int* err_flag = nullptr;
     uint8_t* staging = nullptr;              // uint8 local slab (set/get_config from host)
     uint64_t* ghost_snap = nullptr;          // [2 rows][nplanes] snapshot / delta buffers (world > 1)
@@ -450,6 +451,7 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     // regimes are instruction-issue bound, not load-latency bound); it stays selectable
     if (use_tile && mode == KMC_KERNEL_AUTO) use_tile = false;
     cudaError_t le = use_tile ? launch_substep_tile(a, c->stream) : cudaErrorNotSupported;
+    if (le == cudaSuccess && use_tile) le = queue_slot_reset(a, c->stream);
     if (le == cudaErrorNotSupported) le = launch_substep(c->kind, a, nactive, c->stream);
     CUDA_TRY(c, le);
     if (c->timing) CUDA_TRY(c, cudaEventRecord(e1, c->stream));
@@ -820,8 +822,10 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     ok = ok && alloc((void**)&c->wev, (size_t)owned * 4);
     ok = ok && alloc((void**)&c->wmark, (size_t)owned * 4);
     ok = ok && alloc((void**)&c->ev_total, 8);
-    ok = ok && alloc((void**)&c->queue, 8);
+    ok = ok && alloc((void**)&c->queue, 8) && cudaMemsetAsync(c->queue, 0, 8, c->stream) == cudaSuccess;
     ok = ok && alloc((void**)&c->obs_buf, KMC_OBS_WORDS * 8);
+    ok = ok && alloc((void**)&c->obs_acc, (kObsCounters + 1) * 8) &&
+         cudaMemsetAsync(c->obs_acc, 0, (kObsCounters + 1) * 8, c->stream) == cudaSuccess;
     ok = ok && alloc((void**)&c->err_flag, 4);
     if (g.ghost) {
         ok = ok && alloc((void**)&c->ghost_snap, (size_t)4 * g.R * g.Mx * 8);
@@ -874,7 +878,7 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
     cudaFree(c->flags);
-    cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->err_flag);
+    cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->obs_acc); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv); cudaFree(c->series);
     cudaFree(c->spare[0]); cudaFree(c->spare[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);
@@ -1381,9 +1385,9 @@ kmc_status kmc_vgroup_run_nested(kmc_ctx** cs, int32_t world, double T, double d
 static kmc_status enqueue_obs(kmc_ctx* c, unsigned long long* out) {
     kmc_status st = exchange_forward(c);   // ghosts current for the +y bonds of the last owned row
     if (st != KMC_OK) return st;
-    CUDA_TRY(c, cudaMemsetAsync(out, 0, KMC_OBS_WORDS * 8, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(out + kObsCounters, c->ev_total, 8, cudaMemcpyDeviceToDevice, c->stream));
     ObsArgs a{};
+    a.acc = c->obs_acc;
+    a.ev_total = c->ev_total;
     a.g = c->g;
     a.plane0 = c->planes[0];
     a.plane1 = c->planes[1];

@@ -38,7 +38,7 @@ struct SubstepArgs {
     uint64_t* plane1;
     uint32_t* wev;                   // cumulative events per owned cell [My_local][R][Mx]
     unsigned long long* ev_total;    // device event counter
-    unsigned int* queue;             // dynamic chunk counter of the persistent window kernel
+    unsigned int* queue;             // [2] chunk counters of the persistent window kernel: window w uses [w & 1]
     int colour, C;
     double D;                        // window duration
     double inv_scale;                // 2^-F
@@ -78,6 +78,8 @@ struct ObsArgs {
     unsigned long long* out;         // [4 n_state][16 by_colour][16 nn ordered], then events, windows, time
     unsigned long long windows;      // written to out[37] / out[38] by one thread (host values at enqueue)
     double time;
+    unsigned long long* acc;         // [kObsCounters + 1] self-cleaning accumulator + block ticket (zero between calls)
+    const unsigned long long* ev_total;
 };
 
 constexpr int kObsCounters = 4 + 16 + 16;
@@ -116,6 +118,7 @@ cudaError_t launch_series_hist(const unsigned long long* series, long long first
 // kernels.cu
 cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cudaStream_t s);
 cudaError_t launch_substep_tile(const SubstepArgs& a, cudaStream_t s);   // kmc_tile.cu (2D spin flip)
+cudaError_t queue_slot_reset(const SubstepArgs& a, cudaStream_t s);
 cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s);
 cudaError_t launch_pack(const Geo& g, const uint8_t* in, uint64_t* p0, uint64_t* p1, int nstates,
                         unsigned int* err, cudaStream_t s);

@@ -133,6 +133,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     __shared__ uint8_t s_sel8[kSel8];
     for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = make_double2(a.log_c[i], a.log_l[i]);
     init_sel8(s_sel8);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // the next window's counter
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -267,7 +268,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
             uint32_t nb = 0, nend = 0;
             bool claimed = false;
             if (need > avail && pool_open) {                       // warp-uniform: claim a chunk
-                if (lane == 0) nb = atomicAdd(a.queue, chunk);
+                if (lane == 0) nb = atomicAdd(a.queue + (a.w_lo & 1u), chunk);
                 const unsigned long long base = pool0 + __shfl_sync(FULL, nb, 0);
                 claimed = base < nactive;
                 pool_open = claimed;
@@ -319,15 +320,21 @@ static cudaError_t launch_v(const SubstepArgs& a, long long nactive, cudaStream_
     const long long want = (nactive + chunk - 1) / chunk;          // warps if every warp took one chunk
     const long long nwarps = want < cap_warps ? want : cap_warps;
     const unsigned nb = (unsigned)((nwarps * 32 + bs - 1) / bs);
-    cudaError_t e = cudaMemsetAsync(a.queue, 0, sizeof(unsigned int), s);
-    if (e != cudaSuccess) return e;
+    // no memset per window: the chunk counter is a.queue[w & 1], zeroed by the previous window
+    // (queue_slot_reset); this kernel zeroes the other slot for the next window
     kern<<<nb, bs, 0, s>>>(a, (uint32_t)nactive, (uint32_t)chunk);
     return cudaGetLastError();
 }
 
+// a window that does not run substep_kernel (no active cells, or the tile kernel) zeroes the next
+// window's chunk counter itself
+cudaError_t queue_slot_reset(const SubstepArgs& a, cudaStream_t s) {
+    return cudaMemsetAsync(a.queue + ((a.w_lo & 1u) ^ 1u), 0, sizeof(unsigned int), s);
+}
+
 template <int KIND, int NDIM>
 static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
-    if (nactive <= 0) return cudaSuccess;
+    if (nactive <= 0) return queue_slot_reset(a, s);
     // launch shape experiments: KMC_LB=3 forces the 128-register build, KMC_LB=4 the 80-register one,
     // KMC_LB=6 the 80-register spin-flip build; KMC_MH=1 merged halo boards for spin flip
     static const int lb = [] { const char* e = getenv("KMC_LB"); return e ? atoi(e) : 0; }();
@@ -396,11 +403,8 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
     constexpr int NS = NP + 1;
     const Geo& g = a.g;
     __shared__ unsigned long long sh[kObsCounters];
+    __shared__ bool last;
     for (int i = threadIdx.x; i < kObsCounters; i += blockDim.x) sh[i] = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.out[kObsCounters + 1] = a.windows;
-        a.out[kObsCounters + 2] = (unsigned long long)__double_as_longlong(a.time);
-    }
     __syncthreads();
     uint32_t acc[kObsCounters];
 #pragma unroll
@@ -464,7 +468,25 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kObsCounters; i += blockDim.x)
-        if (sh[i]) atomicAdd(&a.out[i], sh[i]);
+        if (sh[i]) atomicAdd(&a.acc[i], sh[i]);
+    // the last block to finish moves the totals to `out` (no memset / copy launches per call) and
+    // leaves the accumulator and the ticket zero for the next call
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&a.acc[kObsCounters], 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < kObsCounters; i += blockDim.x) {
+        a.out[i] = atomicExch(&a.acc[i], 0ull);
+    }
+    if (threadIdx.x == 0) {
+        a.out[kObsCounters] = *(volatile const unsigned long long*)a.ev_total;
+        a.out[kObsCounters + 1] = a.windows;
+        a.out[kObsCounters + 2] = (unsigned long long)__double_as_longlong(a.time);
+        a.out[kObsCounters + 3] = 0ull;
+        a.acc[kObsCounters] = 0ull;
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
