@@ -1,6 +1,6 @@
 # every workload's bench line (N=1) + the reference arm; JSON lines to gpurun_out/bench_<name>.json
 mkdir -p gpurun_out
-for w in "ising2d_32768" "ising2d_32768:0.01" "zgb2d_32768" "diff2d_8192" "ising2d_1024" "ising1d_65536"; do
+for w in "ising2d_32768" "ising2d_32768:0.01" "zgb2d_32768" "diff2d_8192" "ising2d_1024" "ising1d_65536" "ising1d_65536x64" "noninteracting1d_1024x1000"; do
   wl=${w%%:*}; dt=${w#*:}; [ "$dt" = "$w" ] && dt=""
   name=$wl${dt:+_dt$dt}
   extra=""; [ "$wl" != "ising2d_32768" ] || [ -n "$dt" ] && extra="--no-cpu-baseline"
