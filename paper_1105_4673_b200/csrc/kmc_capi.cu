@@ -427,6 +427,11 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
         }
         static const int hop_env = [] { const char* e = getenv("KMC_HOPFAST"); return e ? atoi(e) : 1; }();
         if (!hop_env) a.hop_fast = 0;
+    } else if (c->kind == KMC_ZGB || c->kind == KMC_ZGB_DIFF) {   // one rate per direction group
+        const int z = 2 * c->g.ndim;
+        a.hop_fast = 1;
+        for (int i = 1; i < c->nclass; ++i)
+            a.hop_fast &= a.rate[i] == a.rate[1 + ((i - 1) / z) * z] ? 1 : 0;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {

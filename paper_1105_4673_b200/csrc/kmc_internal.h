@@ -57,7 +57,7 @@ struct SubstepArgs {
     uint32_t w_lo, w_hi_tag;         // window id (tag EVT = 0 in bits 28..31)
     uint64_t rate[kMaxClass];        // u64 fixed-point class rates (R18)
     uint64_t hopz[4];                // ADSDES_DIFF: (z - n) x the hop rate of block n (uniform blocks, R31)
-    int hop_fast;                    // ADSDES_DIFF: every hop block has one rate -> event_step_hop
+    int hop_fast;                    // every hop block (ADSDES_DIFF) / direction group (ZGB) has one rate
     double log_c[kLogTab];           // log_spec tables: c_j = 128/(j+91)
     double log_l[kLogTab];           //   L_j = -log(c_j), host libm
     double lcoef[6];                 //   {1/7, -1/6, 1/5, 1/3, ln2_hi, ln2_lo} (exact hex literals)

@@ -255,6 +255,8 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     for (;;) {
         bool fin;
         if constexpr (KIND == 4) fin = event_step_hop<NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
+        else if constexpr (KIND == 5 || KIND == 6)
+            fin = event_step_zgb_grouped<KIND - 3, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
         else fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
         pend = pend || fin;
         have = have && !fin;
@@ -368,6 +370,16 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
                 return hlb == 2 ? launch_v<4, NDIM, 2, true, false>(a, nactive, s)
                      : hlb == 4 ? launch_v<4, NDIM, 4, true, false>(a, nactive, s)
                                 : launch_v<4, NDIM, 3, true, false>(a, nactive, s);
+            }
+        }
+        if constexpr (KIND == 2 || KIND == 3) {
+            // equal rates within every direction group: the grouped step (KMC_ZGBFAST=0 disables)
+            static const int zf = [] { const char* e = getenv("KMC_ZGBFAST"); return e ? atoi(e) : 1; }();
+            if (a.hop_fast && zf) {
+                constexpr int KG = KIND + 3;
+                if (a.nest) return launch_v<KG, NDIM, 3, true, true>(a, nactive, s);
+                if (NDIM == 2 && a.peer_up[0]) return launch_v<KG, NDIM, 3, true, false, NDIM == 2>(a, nactive, s);
+                return launch_v<KG, NDIM, 3, true, false>(a, nactive, s);
             }
         }
         const bool big = (KIND == 1 && lb != 4) || lb == 3;

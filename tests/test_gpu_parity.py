@@ -363,6 +363,23 @@ def test_multiscale_split_hop_blocks_bit_exact(ndim, dims, cell):
     assert orc.events > 0
 
 
+def test_multiscale_split_zgb_groups_bit_exact():
+    """f2 with a fast set that splits a ZGB direction group (O2 adsorption along x fast, the rest
+    slow): group rates differ within a window, so the windows run the generic ZGB step instead of
+    the grouped one -- bit-exact vs O2 either way."""
+    params = dict(k1=0.45, k2=1.0, c_hop=2.0)
+    gpu, orc = make_pair(2, (32, 64), (4, 8), "zgb_diff", params, 0, 2)
+    lat = si.categorical_lattice(gpu.local_shape, [0.5, 0.3, 0.2], seed=14)
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    fast = [1, 2]                                    # O2 adsorption, directions -x and +x
+    for _ in range(2):
+        gpu.run_multiscale(1.0, 0.5, 2, "lie", fast_classes=sum(1 << c for c in fast))
+        orc.run_multiscale(1.0, 0.5, 2, "lie", fast_classes=fast)
+        assert_same_state(gpu, orc, "multiscale split zgb groups")
+    assert orc.events > 0
+
+
 NESTED = [
     # ndim, dims, cell, kind, params, block, outer, inner, n_inner
     (2, (64, 128), (8, 8), "adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), 2, "lie", "lie", 2),
