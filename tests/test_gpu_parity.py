@@ -227,23 +227,27 @@ def test_device_buffers_roundtrip():
     assert np.array_equal(g.get_config(), lat)
 
 
-@pytest.mark.parametrize("kind", ["adsdes", "zgb"])
+FULL_SIZE = {"adsdes": "ising2d_32768", "zgb": "zgb2d_32768", "adsdes_diff": "diff2d_8192"}
+
+
+@pytest.mark.parametrize("kind", list(FULL_SIZE))
 def test_full_size_sampled_cells(kind):
-    """BASELINE target size 32768^2 in the launch configuration bench.py times: one window on
-    the GPU; 512 sampled active cells recomputed by the oracle from the pre-window lattice
-    (cells of one colour are independent within a window, eq.(exact))."""
+    """The bench workloads at full size (BASELINE target 32768^2, ZGB 32768^2, diffusion 8192^2) in
+    the launch configuration bench.py times: one window on the GPU; 512 sampled active cells
+    recomputed by the oracle from the pre-window lattice (cells of one colour are independent
+    within a window, eq.(exact))."""
     torch = _cuda()
     import paper_1105_4673_b200 as kmc
-    wl = dict(si.WORKLOADS["ising2d_32768" if kind == "adsdes" else "zgb2d_32768"])
+    wl = dict(si.WORKLOADS[FULL_SIZE[kind]])
     H, W = wl["dims"]
     qy, qx = wl["cell"]
     g = kmc.KMC(2, (H, W), (qy, qx), kind=kind, seed=99, **wl["params"])
-    if kind == "adsdes":
+    if kind.startswith("adsdes"):
         lat = si.bernoulli_lattice((1, H, W), 0.5, seed=si.SEED_BASE)
     else:
         lat = si.categorical_lattice((1, H, W), [0.5, 0.25, 0.25], seed=si.SEED_BASE)
     g.set_config(lat)
-    g.run(2.0 * wl["dt"], wl["dt"], "lie")       # advance a little so the state is not the input
+    g.run(2.0 * wl["dt"], wl["dt"], wl["scheme"])   # advance a little so the state is not the input
     pre = g.get_config()
     w0, _ = g.get_state()
     ev_pre = g.observables(per_cell=True)["per_cell_events"][0]
