@@ -353,6 +353,11 @@ def main():
             "per_unit": f"{ipe} warp-inst/event (ncu sm__inst_executed / events, profiles/substep_profile.json)",
             "traffic": pent.get("dram_bytes_per_launch") if ipe else None,
             "profile_key": pkey if ipe else None,
+            # the binding pipe (ncu capture of one window of this workload): the ALU pipe issues at
+            # half the warp-instruction rate and carries ~half the instructions of an event step
+            "ncu_pipes": ({"alu_pipe_pct": pent.get("alu_pipe_pct"), "xu_pipe_pct": pent.get("xu_pipe_pct"),
+                           "fp64_pipe_pct": pent.get("fp64_pipe_pct"), "issue_active_pct": pent.get("issue_active_pct")}
+                          if ipe else None),
             "kernel": "substep_kernel", "avg_launch_ms": avg_launch_ms, "launches": launches,
             "kernel_share_of_step": kern_ms / ms,
             "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
