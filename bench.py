@@ -176,7 +176,7 @@ def main():
     ap.add_argument("--workload", default="ising2d_32768", choices=sorted(si.WORKLOADS))
     ap.add_argument("--dt", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: one workload-sized slab per GPU (default); strong: the workload split over the GPUs")
     ap.add_argument("--fused-exchange", action="store_true",
