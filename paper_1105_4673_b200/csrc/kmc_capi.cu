@@ -131,6 +131,7 @@ struct kmc_ctx {
     unsigned int* queue = nullptr;           // window kernel's dynamic chunk counter
     unsigned long long* obs_buf = nullptr;   // KMC_OBS_WORDS (enqueue_obs layout)
     unsigned long long* obs_acc = nullptr;   // kObsCounters + 1: the observables kernel's accumulator + ticket
+    double2* logtab = nullptr;               // log_spec table {c_j, L_j}
     unsigned int* err_flag = nullptr;
     uint8_t* staging = nullptr;              // uint8 local slab (set/get_config from host)
     uint64_t* ghost_snap = nullptr;          // [2 rows][nplanes] snapshot / delta buffers (world > 1)
@@ -353,10 +354,7 @@ void build_args_template(kmc_ctx* c) {
         a.rk1[i] = a.key1 + (uint32_t)i * 0xBB67AE85u;
     }
     for (int i = 0; i < c->nclass; ++i) a.rate[i] = c->crate_u64[i];
-    for (int j = 0; j < kLogTab; ++j) {   // log_spec tables, host libm
-        a.log_c[j] = 128.0 / (double)(j + 91);
-        a.log_l[j] = -std::log(a.log_c[j]);
-    }
+    a.logtab = c->logtab;
     a.lcoef[0] = 0x1.2492492492492p-3;      // 1/7
     a.lcoef[1] = -0x1.5555555555555p-3;     // -1/6
     a.lcoef[2] = 0x1.999999999999ap-3;      // 1/5
@@ -829,6 +827,15 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     ok = ok && alloc((void**)&c->ev_total, 8);
     ok = ok && alloc((void**)&c->queue, 8) && cudaMemsetAsync(c->queue, 0, 8, c->stream) == cudaSuccess;
     ok = ok && alloc((void**)&c->obs_buf, KMC_OBS_WORDS * 8);
+    ok = ok && alloc((void**)&c->logtab, kLogTab * sizeof(double2));
+    if (ok) {   // log_spec tables, host libm; uploaded once
+        double2 tab[kLogTab];
+        for (int j = 0; j < kLogTab; ++j) {
+            tab[j].x = 128.0 / (double)(j + 91);
+            tab[j].y = -std::log(tab[j].x);
+        }
+        ok = cudaMemcpy(c->logtab, tab, sizeof tab, cudaMemcpyHostToDevice) == cudaSuccess;
+    }
     ok = ok && alloc((void**)&c->obs_acc, (kObsCounters + 1) * 8) &&
          cudaMemsetAsync(c->obs_acc, 0, (kObsCounters + 1) * 8, c->stream) == cudaSuccess;
     ok = ok && alloc((void**)&c->err_flag, 4);
@@ -883,7 +890,7 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
     cudaFree(c->flags);
-    cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->obs_acc); cudaFree(c->err_flag);
+    cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->obs_acc); cudaFree(c->logtab); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv); cudaFree(c->series);
     cudaFree(c->spare[0]); cudaFree(c->spare[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);

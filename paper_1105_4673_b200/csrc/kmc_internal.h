@@ -58,8 +58,9 @@ struct SubstepArgs {
     uint64_t rate[kMaxClass];        // u64 fixed-point class rates (R18)
     uint64_t hopz[4];                // ADSDES_DIFF: (z - n) x the hop rate of block n (uniform blocks, R31)
     int hop_fast;                    // every hop block (ADSDES_DIFF) / direction group (ZGB) has one rate
-    double log_c[kLogTab];           // log_spec tables: c_j = 128/(j+91)
-    double log_l[kLogTab];           //   L_j = -log(c_j), host libm
+    const double2* logtab;           // log_spec table {c_j, L_j}, kLogTab entries in device
+                                     // memory: c_j = 128/(j+91), L_j = -log(c_j) (host libm); kept out of
+                                     // the parameters so a launch copies ~0.8 KB instead of ~2.3 KB
     double lcoef[6];                 //   {1/7, -1/6, 1/5, 1/3, ln2_hi, ln2_lo} (exact hex literals)
     // fused halo exchange (SURVEY §8(e) "later option"): the window kernel mirrors every write to a
     // boundary-row or ghost-row word into the neighbour ranks' planes (peer pointers: other slabs on

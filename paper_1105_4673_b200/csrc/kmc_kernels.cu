@@ -131,7 +131,7 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     // log_spec tables -> shared memory (lanes index them by their own bucket)
     __shared__ double2 s_logt[kLogTab];
     __shared__ uint8_t s_sel8[kSel8];
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = make_double2(a.log_c[i], a.log_l[i]);
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
     init_sel8(s_sel8);
     if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // the next window's counter
     __syncthreads();

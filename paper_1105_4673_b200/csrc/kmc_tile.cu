@@ -38,7 +38,7 @@ tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
     const uint32_t rowlen = (uint32_t)g.R * g.Mx;
     const uint32_t rbase = (uint32_t)r * g.Mx;
 
-    for (int i = tid; i < kLogTab; i += blockDim.x) s_logt[i] = make_double2(a.log_c[i], a.log_l[i]);
+    for (int i = tid; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
     init_sel8(s_sel8);
     if (tid == 0) s_next = blockDim.x;
     // a3: the tile and its halo ring, row by row (coalesced), periodic wrap / ghost rows
