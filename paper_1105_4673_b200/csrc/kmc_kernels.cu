@@ -130,9 +130,10 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     const unsigned FULL = 0xffffffffu;
     // log_spec tables -> shared memory (lanes index them by their own bucket)
     __shared__ double2 s_logt[kLogTab];
-    __shared__ uint8_t s_sel8[kSel8];
+    __shared__ __align__(16) uint8_t s_sel8[kSel8 + kDirTab];     // sel8 table + direction table
     for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
     init_sel8(s_sel8);
+    if constexpr (KIND != 0) init_dirtab(s_sel8, g);
     if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // the next window's counter
     __syncthreads();
     const int lane = threadIdx.x & 31;
