@@ -439,6 +439,8 @@ class _Rank(KMC):
         self.local_shape = (rl.value, hl.value, w.value)
         self.replica_offset, self.row_offset = ro.value, yo.value
         self.nbytes = rl.value * hl.value * w.value
+        qy, qx = (1, int(geom.cell[0])) if int(geom.ndim) == 1 else (int(geom.cell[0]), int(geom.cell[1]))
+        self.packed_shape = (2 if self.nstates == 3 else 1, hl.value // qy, rl.value, w.value // qx)
 
 
 def _partition(L, check, fn, ctx, parts, granule, nstrips):

@@ -574,6 +574,37 @@ def test_staged_config_pipelined_upload(kind, dims, cell, params):
         assert np.array_equal(a.get_config(), lat1)
 
 
+@pytest.mark.parametrize("fused", [False, True])
+def test_staged_config_on_virtual_ranks(fused):
+    """The pipelined upload on the slabs of a virtual-rank group (ghost rows kept defined at the
+    commit, refreshed by the next exchange; with the fused exchange the commit copies into the
+    IPC-stable planes): identical to G = 1 with a synchronous upload."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)
+    one = kmc.KMC(2, (64, 32), (8, 8), kind="adsdes", replicas=2, seed=6, **p)
+    grp = kmc.VGroup(4, (64, 32), (8, 8), kind="adsdes", replicas=2, seed=6, **p)
+    if fused:
+        grp.set_fused(True)
+    lat1 = si.bernoulli_lattice(one.local_shape, 0.5, seed=1)
+    lat2 = si.bernoulli_lattice(one.local_shape, 0.3, seed=2)
+    one.set_config(lat1)
+    grp.set_config(lat1)
+    one.run(2.0, 1.0)
+    grp.run(2.0, 1.0)
+    for rk in grp.ranks:
+        h = rk.local_shape[1]
+        rk.stage_config_packed(_pack_words(lat2[:, rk.row_offset:rk.row_offset + h], 8, 8, 1))
+    for rk in grp.ranks:
+        rk.commit_config()
+    one.set_config(lat2)
+    assert np.array_equal(grp.get_config(), lat2)
+    one.run(3.0, 1.0)
+    grp.run(3.0, 1.0)
+    assert np.array_equal(one.get_config(), grp.get_config())
+    assert one.observables()["events"] == grp.observables()["events"]
+
+
 def _half_full(shape):
     lat = np.zeros(shape, dtype=np.uint8)
     lat[:, : shape[1] // 2] = 1                 # top half full: few events; bottom half empty: many
