@@ -162,23 +162,25 @@ def test_cfg1_noninteracting_acf_and_distribution_closed_form():
 
 
 def test_1d_ising_acf_vs_exact_ssa():
-    """1D Ising (Fig. autocorr1D: beta = 4, h_paper = 1, R9 h_dyn = h_paper - 2K), N = 64, Q = 8:
-    the GPU's coverage autocorrelation at Lie dt = 0.05 vs the exact SSA's (O1, sampled at the same
-    times), both at stationarity, within Z SE + the O(dt) splitting bias allowance 0.03."""
+    """1D Ising (Fig. autocorr1D: beta = 4, h_paper = 1, R9 h_dyn = h_paper - 2K), N = 64, Q = 8: the
+    coverage autocorrelation of the GPU's process at Lie dt = 0.1, sampled every 0.5 time units
+    after a burn-in of 50, vs the exact SSA's (O1) at the same times, for lags 0.5 .. 8 (the acf
+    decays from ~0.96 to ~0.55 there): within Z SE of the difference (replica-batch SEs)."""
     kmc = _kmc()
-    N, q, M, dt, burn, nobs = 64, 8, 400, 0.05, 40, 60
+    N, q, dt, burn, stride, nobs = 64, 8, 0.1, 50.0, 5, 80
     prm = dict(ca=1.0, cd=1.0, beta=4.0, K=1.0, h=1.0 - 2.0)
-    L = 12
+    lags = (1, 2, 4, 8, 16)
+    L = max(lags)
+    M, Ms = 800, 400
     g = kmc.KMC(1, (N,), (q,), kind="adsdes", replicas=M, seed=8, **prm)
     g.set_config(si.bernoulli_lattice(g.local_shape, 0.5, seed=4))
-    g.run(burn * dt * 10, dt * 10, "lie")                      # burn-in (coarse steps are fine)
-    g.record_coverage(nobs + 1)
-    g.run(nobs * dt * 2, dt, "lie")                            # 2 nobs macro-steps: keep the first nobs+1
-    gpu = g.coverage_series()[: nobs + 1]
-    Ms = 160
+    g.run(burn, 1.0, "lie")                                   # burn-in (coarse steps)
+    g.record_coverage(nobs * stride + 1)
+    g.run(nobs * stride * dt, dt, "lie")
+    gpu = g.coverage_series()[::stride][: nobs + 1]
     ssa = np.zeros((nobs + 1, Ms), dtype=np.int64)
     lat0 = si.bernoulli_lattice((Ms, 1, N), 0.5, seed=12)
-    times = [burn * dt * 10 + i * dt for i in range(nobs + 1)]
+    times = [burn + i * stride * dt for i in range(nobs + 1)]
     for r in range(Ms):
         snaps, _ = ssa_snapshots(lat0[r], 1, "adsdes", model_params(**prm), times, seed=99, stream=r)
         ssa[:, r] = snaps.reshape(nobs + 1, -1).sum(axis=1)
@@ -189,6 +191,7 @@ def test_1d_ising_acf_vs_exact_ssa():
         return full, parts.std(axis=0, ddof=1) / np.sqrt(nb)
 
     ag, sg = acf_se(gpu, 10)
-    as_, ss = acf_se(ssa, 8)
-    for l in (1, 2, 4, 8, 12):
-        assert abs(ag[l] - as_[l]) < Z * np.hypot(sg[l], ss[l]) + 0.03, (l, ag[l], as_[l], sg[l], ss[l])
+    as_, ss = acf_se(ssa, 10)
+    assert as_[L] < 0.8 and ag[1] > 0.9                       # the lags span the decay
+    for l in lags:
+        assert abs(ag[l] - as_[l]) < Z * np.hypot(sg[l], ss[l]), (l, ag[l], as_[l], sg[l], ss[l])
