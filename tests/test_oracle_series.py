@@ -7,6 +7,8 @@
   the scheme's own macro-step chain P = e^{dt Q^0} e^{dt Q^1} at stationarity.
 Statistical comparisons use Z = 4.5 standard errors from replica batches.
 """
+import math
+
 import numpy as np
 import pytest
 from scipy.linalg import expm
@@ -124,3 +126,23 @@ def test_binomial_pmf_is_a_law():
     p = series.binomial_pmf(30, 0.3)
     assert p.sum() == pytest.approx(1.0, abs=1e-12)
     assert (np.arange(31) * p).sum() == pytest.approx(9.0, abs=1e-10)
+
+
+def test_init_random_law_and_special_cases():
+    """R32 initial configurations: frequencies within Z SE of p (3 states, 20k sites); p = (1, 0)
+    gives the empty lattice and p = (0, 1) the full one exactly; the state of a site depends on its
+    global coordinates only (a slab of rows / replicas equals the slice of the whole lattice)."""
+    from oracle.init import init_random, thresholds
+    p = (0.5, 0.3, 0.2)
+    lat = init_random(5, 40, 100, p, seed=0x5EED)
+    for s, ps in enumerate(p):
+        f = (lat == s).mean()
+        assert abs(f - ps) < Z * math.sqrt(ps * (1 - ps) / lat.size), (s, f)
+    assert not init_random(1, 4, 8, (1.0, 0.0), seed=3).any()
+    assert init_random(1, 4, 8, (0.0, 1.0), seed=3).all()
+    assert thresholds((0.25, 0.75)) == [1 << 30] and thresholds((1.0, 0.0)) == [1 << 32]
+    whole = init_random(3, 8, 16, (0.4, 0.6), seed=11)
+    part = init_random(2, 3, 16, (0.4, 0.6), seed=11, row_offset=4, rep_offset=1)
+    assert np.array_equal(part, whole[1:3, 4:7])
+    with pytest.raises(ValueError):
+        thresholds((0.7, 0.6, 0.1))
