@@ -126,6 +126,14 @@ kmc_status kmc_local_shape(const kmc_ctx* ctx, int64_t* replicas_local, int64_t*
 
 /* Copy the local slab in (validating spin values < number of states, else KMC_EINVAL and the
  * lattice is unchanged) or out.  nbytes must equal replicas_local*rows_local*W.  Synchronous. */
+/* Random initial configuration on the device (no upload; SURVEY §2.3 init kernel, reading R32):
+ * every owned site (x, y) of replica r takes state s with probability probs[s] (nprobs = the
+ * model's number of states; probs >= 0, partial sums <= 1, the last state takes the rest):
+ * s = #{j < nprobs-1 : u >= T_j}, u = word 0 of Philox4x32-10((x, y, r, 2 << 28), key = seed),
+ * T_j = floor(2^32 (probs[0] + .. + probs[j])), 2^32 once the sum reaches 1.  A site's state depends
+ * on (seed, global coordinates) only: identical for any rank split.  Stream-ordered, asynchronous;
+ * KMC_EINVAL on bad probabilities, KMC_ESTATE while a staged upload is pending. */
+kmc_status kmc_init_random(kmc_ctx* ctx, const double* probs, int32_t nprobs, uint64_t seed);
 kmc_status kmc_set_config(kmc_ctx* ctx, const uint8_t* host_local_slab, int64_t nbytes);
 kmc_status kmc_get_config(kmc_ctx* ctx, uint8_t* host_local_slab, int64_t nbytes);
 /* Same with a device buffer (e.g. a torch CUDA tensor), stream-ordered, no validation report

@@ -34,6 +34,7 @@ EXPORTS = [
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
     "kmc_vgroup_set_fused", "kmc_abi_sizes", "kmc_record_coverage", "kmc_coverage_series", "kmc_coverage_stats",
     "kmc_stage_config_packed", "kmc_commit_config", "kmc_observables_device", "kmc_obs_decode",
+    "kmc_init_random",
 ]
 OBS_WORDS = 40
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
@@ -122,6 +123,7 @@ def lib():
         "kmc_record_coverage": ([vp, i32, i64], i32),
         "kmc_stage_config_packed": ([vp, vp, i64], i32),
         "kmc_observables_device": ([vp, vp], i32),
+        "kmc_init_random": ([vp, vp, i32, u64], i32),
         "kmc_obs_decode": ([vp, vp, P(KmcObs)], i32),
         "kmc_commit_config": ([vp], i32),
         "kmc_coverage_series": ([vp, vp, i64, P(i64)], i32),
@@ -245,6 +247,11 @@ class KMC:
         out = np.empty(self.local_shape, dtype=np.uint8)
         self._check(self._L.kmc_get_config(self._ctx, out.ctypes.data, out.size))
         return out
+
+    def init_random(self, probs, seed=0):
+        """kmc_init_random: i.i.d. site states with probabilities `probs` drawn on the device (R32)."""
+        p = np.ascontiguousarray(probs, dtype=np.float64)
+        self._check(self._L.kmc_init_random(self._ctx, p.ctypes.data, int(p.size), int(seed) & 0xFFFFFFFFFFFFFFFF))
 
     def set_config_packed(self, words):
         """Host uint64 words in packed_shape (kmc_set_config_packed: 1 bit per site and plane)."""

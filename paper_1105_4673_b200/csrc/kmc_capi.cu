@@ -953,6 +953,25 @@ kmc_status kmc_get_config_device(kmc_ctx* c, uint8_t* dev, int64_t nbytes) {
     return KMC_OK;
 }
 
+kmc_status kmc_init_random(kmc_ctx* c, const double* probs, int32_t nprobs, uint64_t seed) {
+    if (!c || !probs) return fail(c, KMC_EINVAL, "NULL argument");
+    if (c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
+    if (nprobs != c->nstates) return fail(c, KMC_EINVAL, "need %d probabilities, got %d", c->nstates, nprobs);
+    unsigned long long thr[2] = {0, 0};
+    double cum = 0.0;
+    for (int j = 0; j < nprobs; ++j)
+        if (!(probs[j] >= 0.0) || std::isinf(probs[j])) return fail(c, KMC_EINVAL, "probabilities must be finite and >= 0");
+    for (int j = 0; j + 1 < nprobs; ++j) {   // R32: T_j = floor(2^32 (p_0 + .. + p_j)), 2^32 once the sum reaches 1
+        cum = cum + probs[j];
+        if (cum > 1.0 + 1e-12) return fail(c, KMC_EINVAL, "partial sums of the probabilities exceed 1");
+        thr[j] = cum >= 1.0 ? (1ull << 32) : (unsigned long long)std::floor(cum * 4294967296.0);
+    }
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, launch_init_random(c->g, c->planes[0], c->nplanes > 1 ? c->planes[1] : nullptr, seed, thr,
+                                   nprobs - 1, c->stream));
+    return KMC_OK;
+}
+
 kmc_status kmc_set_config(kmc_ctx* c, const uint8_t* host, int64_t nbytes) {
     if (c && c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
     if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");

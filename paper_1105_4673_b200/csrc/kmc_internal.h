@@ -125,6 +125,8 @@ cudaError_t launch_pack(const Geo& g, const uint8_t* in, uint64_t* p0, uint64_t*
                         unsigned int* err, cudaStream_t s);
 cudaError_t launch_unpack(const Geo& g, const uint64_t* p0, const uint64_t* p1, int nplanes,
                           uint8_t* out, cudaStream_t s);
+cudaError_t launch_init_random(const Geo& g, uint64_t* p0, uint64_t* p1, uint64_t seed, const unsigned long long* thr,
+                               int nthr, cudaStream_t s);
 cudaError_t launch_check_packed(const uint64_t* p0, const uint64_t* p1, long long n, uint64_t valid,
                                 unsigned int* err, cudaStream_t s);
 cudaError_t launch_strip_loads(const Geo& g, const uint32_t* wev, const uint32_t* mark, unsigned long long* strips,

@@ -987,6 +987,64 @@ __global__ void check_packed_kernel(const uint64_t* __restrict__ p0, const uint6
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Random initial configuration (reading R32): site (x, y) of replica r takes
+// state #{j : u >= T_j}, u = word 0 of Philox4x32-10((x, y, r, TAG_INIT << 28), seed).  One thread
+// per owned cell writes the cell's bit-plane words; the state of a site depends on its global
+// coordinates only (identical for any rank split).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t philox_keyed_w0(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                    uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int rd = 0; rd < 10; ++rd) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c0;
+}
+
+__global__ void __launch_bounds__(256) init_random_kernel(const Geo g, uint64_t* p0, uint64_t* p1, uint32_t k0,
+                                                          uint32_t k1, unsigned long long t0, unsigned long long t1,
+                                                          int nthr) {
+    const uint32_t rowlen = (uint32_t)g.R * g.Mx;
+    const long long ncell = (long long)g.My_local * rowlen;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
+         t += (long long)gridDim.x * blockDim.x) {
+        const uint32_t cx = (uint32_t)(t % g.Mx);
+        const uint32_t r = (uint32_t)((t / g.Mx) % g.R);
+        const uint32_t cy = (uint32_t)(t / rowlen);
+        const uint32_t y0 = (uint32_t)(g.row_offset + (int)cy) * (uint32_t)g.qy;
+        uint64_t w0 = 0, w1 = 0;
+        for (int ly = 0; ly < g.qy; ++ly)
+            for (int lx = 0; lx < g.qx; ++lx) {
+                const uint32_t u = philox_keyed_w0(cx * (uint32_t)g.qx + (uint32_t)lx, y0 + (uint32_t)ly,
+                                                   (uint32_t)g.rep_offset + r, 2u << 28, k0, k1);
+                const int st = (nthr > 0 && u >= t0 ? 1 : 0) + (nthr > 1 && u >= t1 ? 1 : 0);
+                const uint64_t bit = 1ull << (ly * g.qx + lx);
+                w0 |= st == 1 ? bit : 0ull;
+                w1 |= st == 2 ? bit : 0ull;
+            }
+        const size_t idx = (size_t)(cy + (uint32_t)g.ghost) * rowlen + (size_t)r * g.Mx + cx;
+        p0[idx] = w0;
+        if (p1) p1[idx] = w1;
+    }
+}
+
+cudaError_t launch_init_random(const Geo& g, uint64_t* p0, uint64_t* p1, uint64_t seed, const unsigned long long* thr,
+                               int nthr, cudaStream_t s) {
+    const long long ncell = (long long)g.My_local * g.R * g.Mx;
+    if (ncell <= 0) return cudaSuccess;
+    long long nb = (ncell + 255) / 256;
+    if (nb > 148LL * 32) nb = 148LL * 32;
+    init_random_kernel<<<(unsigned)nb, 256, 0, s>>>(g, p0, p1, (uint32_t)seed, (uint32_t)(seed >> 32),
+                                                    nthr > 0 ? thr[0] : 0ull, nthr > 1 ? thr[1] : 0ull, nthr);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_packed(const uint64_t* p0, const uint64_t* p1, long long n, uint64_t valid,
                                 unsigned int* err, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

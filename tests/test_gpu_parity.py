@@ -605,6 +605,42 @@ def test_staged_config_on_virtual_ranks(fused):
     assert one.observables()["events"] == grp.observables()["events"]
 
 
+@pytest.mark.parametrize("ndim,dims,cell,kind,R,probs", [
+    (1, (256,), (16,), "adsdes", 3, (0.6, 0.4)),
+    (2, (32, 48), (4, 8), "zgb", 2, (0.5, 0.3, 0.2)),
+    (2, (24, 40), (2, 4), "adsdes_diff", 1, (0.0, 1.0)),
+])
+def test_init_random_matches_oracle(ndim, dims, cell, kind, R, probs):
+    """kmc_init_random (device, R32) == oracle/init.py site by site; a run from it == a run of O2
+    from the same lattice."""
+    from oracle.init import init_random
+    gpu, orc = make_pair(ndim, dims, cell, kind, {}, 0, R)
+    gpu.init_random(probs, seed=0xC0FFEE)
+    H, W = (1, dims[0]) if ndim == 1 else dims
+    ref = init_random(R, H, W, probs, 0xC0FFEE)
+    assert np.array_equal(gpu.get_config(), ref)
+    orc.set_config(ref)
+    gpu.run(1.0, 0.5, "lie")
+    orc.run(1.0, 0.5, "lie")
+    assert_same_state(gpu, orc, "after init_random")
+
+
+def test_init_random_virtual_ranks_and_errors():
+    """Each virtual rank fills its own slab; together they equal G = 1 (global site ids)."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    one = kmc.KMC(2, (64, 32), (8, 8), kind="adsdes", replicas=2, seed=1)
+    grp = kmc.VGroup(4, (64, 32), (8, 8), kind="adsdes", replicas=2, seed=1)
+    one.init_random((0.35, 0.65), seed=7)
+    for rk in grp.ranks:
+        rk.init_random((0.35, 0.65), seed=7)
+    assert np.array_equal(one.get_config(), grp.get_config())
+    with pytest.raises(kmc.KmcError):
+        one.init_random((0.5, 0.3, 0.2), seed=1)           # adsdes has 2 states
+    with pytest.raises(kmc.KmcError):
+        one.init_random((-0.1, 1.1), seed=1)
+
+
 def _half_full(shape):
     lat = np.zeros(shape, dtype=np.uint8)
     lat[:, : shape[1] // 2] = 1                 # top half full: few events; bottom half empty: many
