@@ -1641,6 +1641,10 @@ kmc_status kmc_get_state(const kmc_ctx* c, uint64_t* windows, double* time) {
 
 kmc_status kmc_set_state(kmc_ctx* c, uint64_t windows, double time) {
     if (!c) return KMC_EINVAL;
+    // the window kernel's chunk counters alternate with the window parity (window w claims from
+    // slot w & 1 and zeroes the other); an arbitrary new counter may repeat the last parity
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemsetAsync(c->queue, 0, 2 * sizeof(unsigned int), c->stream));
     c->window = windows;
     c->time = time;
     return KMC_OK;

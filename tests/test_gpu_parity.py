@@ -188,6 +188,27 @@ def test_resume_run_split_equals_whole():
     assert np.array_equal(a.get_config(), c.get_config())
 
 
+def test_set_state_same_parity_after_claimed_chunks():
+    """Restoring a window counter of the same parity as the last window (kmc_set_state) after a
+    window whose warps claimed chunks from the dynamic pool (8192^2: more active cells than one
+    chunk per resident warp): the next window still covers every cell -- identical to a fresh
+    context restored to the same state."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)
+    a = kmc.KMC(2, (8192, 8192), (8, 8), kind="adsdes", seed=3, **p)
+    a.init_random((0.5, 0.5), seed=1)
+    a.substep(0, 1.0)                                  # window 0 (parity 0) claims pool chunks
+    lat = a.get_config()
+    a.set_state(2, 0.0)                                # window 2: parity 0 again
+    a.substep(1, 1.0)
+    b = kmc.KMC(2, (8192, 8192), (8, 8), kind="adsdes", seed=3, **p)
+    b.set_config(lat)
+    b.set_state(2, 0.0)
+    b.substep(1, 1.0)
+    assert np.array_equal(a.get_config(), b.get_config())
+
+
 def test_degenerate_cases():
     import paper_1105_4673_b200 as kmc
     _cuda()
