@@ -48,7 +48,12 @@ template <int NDIM, bool NEST>
 __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     const Geo& g = a.g;
     uint32_t rest, j, rowsel, r;
-    fast_divmod(t, a.half, a.inv_half, rest, j);
+    if ((a.half & (a.half - 1u)) == 0u) {      // warp-uniform: half a power of two -> shift / mask
+        j = t & (a.half - 1u);                  // (+0.6 % at dt = 0.01, where the refill is 37 % of the work)
+        rest = t >> (31 - __clz(a.half));
+    } else {
+        fast_divmod(t, a.half, a.inv_half, rest, j);
+    }
     if (g.R == 1) { rowsel = rest; r = 0; }
     else fast_divmod(rest, (uint32_t)g.R, a.inv_R, rowsel, r);
     uint32_t cy, cx;
