@@ -20,8 +20,17 @@
 // pack / unpack: uint8 site-major <-> bit-packed cell-major.
 #include "kmc_device.cuh"
 
+#include <cassert>
 #include <cstdint>
 #include <cstdlib>
+
+// Debug builds (KMC_NVCC_FLAGS=-DKMC_DEBUG_BOUNDS) check every computed word index against its
+// buffer with a device assert (the bounds check used instead of compute-sanitizer).
+#ifdef KMC_DEBUG_BOUNDS
+#define KMC_BOUNDS(cond) assert(cond)
+#else
+#define KMC_BOUNDS(cond) ((void)0)
+#endif
 
 namespace kmc {
 
@@ -104,6 +113,10 @@ __device__ __forceinline__ CellLoc locate(const SubstepArgs& a, uint32_t t) {
     L.iev = cy * rowlen + rbase + cx;
     L.gid32 = (uint32_t)((unsigned long long)(g.rep_offset + r) * (unsigned long long)g.M_global +
                          (unsigned long long)gy * g.Mx + cx);
+    KMC_BOUNDS(cx < (uint32_t)g.Mx && r < (uint32_t)g.R && cy < (uint32_t)g.My_local);
+    KMC_BOUNDS(L.iC < (uint32_t)(g.My_local + 2 * g.ghost) * rowlen && L.iW < (uint32_t)(g.My_local + 2 * g.ghost) * rowlen &&
+               L.iE < (uint32_t)(g.My_local + 2 * g.ghost) * rowlen && L.iN < (uint32_t)(g.My_local + 2 * g.ghost) * rowlen &&
+               L.iS < (uint32_t)(g.My_local + 2 * g.ghost) * rowlen && L.iev < (uint32_t)g.My_local * rowlen);
     return L;
 }
 
