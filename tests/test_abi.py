@@ -149,3 +149,12 @@ def test_missing_library_fails_loudly(tmp_path):
     env = dict(os.environ, KMC_B200_LIB=str(tmp_path / "missing.so"), PYTHONPATH=ROOT)
     r = subprocess.run(["python", "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
     assert "raised" in r.stdout, (r.stdout, r.stderr)
+
+
+def test_nccl_unique_id_loads_nccl():
+    """kmc_nccl_unique_id dlopens NCCL (torch's or the system's) and returns a 128-byte id; two ids
+    differ (the multi-GPU bootstrap the bench broadcasts through torch.distributed)."""
+    import torch  # noqa: F401  (torch's bundled NCCL is what a launched job resolves)
+    import paper_1105_4673_b200 as kmc
+    a, b = kmc.nccl_unique_id(), kmc.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
