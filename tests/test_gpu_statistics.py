@@ -77,6 +77,29 @@ def test_scheme_law_vs_bruteforce(scheme, dt):
         assert abs(emp.mean() - m) <= Z * math.sqrt(v / R), (scheme, dt, name, emp.mean(), m)
 
 
+def test_lie_error_one_over_q():
+    """eq.(liebound) P:666-669 on the GPU: ring N = 12 (empty start, T = 2, Lie dt = 1), cells of
+    q = 1, 2, 3, 6 sites, 2^19 replicas each: the mean coverage equals the exact Lie law
+    (brute force) within Z SE, and its error against the exact SSA law shrinks as 1/q
+    (error x q within 20 % of the brute-force constant -0.027)."""
+    kmc = _kmc()
+    N, T, R = 12, 2.0, 1 << 19
+    p = dict(ca=1.0, cd=1.0, beta=1.0, K=1.0, h=-1.0)
+    for q in (1, 2, 3, 6):
+        lat = bf.Lattice(1, 1, N, 1, q, 2)
+        Q, Qc, S = bf.generators(dict(kind="adsdes", **p), lat)
+        p0 = bf.point_mass(S, N, [0] * N)
+        f = bf.coverage_values(lat, S)
+        law = bf.law(p0, Q, Qc, "lie", 1.0, T, 2)
+        m, v = law @ f, law @ f ** 2 - (law @ f) ** 2
+        ex = bf.law(p0, Q, Qc, "exact", 0, T, 2) @ f
+        g = kmc.KMC(1, (N,), (q,), kind="adsdes", replicas=R, seed=20 + q, **p)
+        g.run(T, 1.0, "lie")
+        emp = g.observables()["coverage"][1]
+        assert abs(emp - m) <= Z * math.sqrt(v / R), (q, emp, m)
+        assert abs((emp - ex) * q / -0.027 - 1.0) < 0.2, (q, emp - ex)
+
+
 def test_weak_error_orders_lie_vs_strang():
     """Global weak error at T = 2 from the asymmetric start, measured on the GPU against the exact
     generator law: Lie error halves with dt (O(dt)); Strang error is O(dt^2) and far smaller."""

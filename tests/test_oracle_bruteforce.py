@@ -140,6 +140,28 @@ def test_boundary_only_commutator():
     assert np.abs(A @ B - B @ A).max() > 1e-3
 
 
+def test_lie_error_one_over_q_and_random_ratio_P6():
+    """eq.(liebound): the Lie coverage error is O(1/q) -- on the N = 12 ring (c_a = c_d = 1,
+    beta = K = 1, h = -1, empty start, T = 2, dt = 1) error x q is constant to 15 % for q = 1, 2, 3, 6
+    (-0.0303, -0.0133, -0.0088, -0.0044); eq.(pcscompare): the random schedule's
+    error exceeds Lie's by a factor growing with q (dt_Lie ~ q dt_Random)."""
+    N = 12
+    errs, ratios = [], []
+    for q in (1, 2, 3, 6):
+        lat = bf.Lattice(1, 1, N, 1, q, 2)
+        Q, Qc, S = bf.generators(ising(beta=1.0, K=1.0, h=-1.0), lat)
+        p0 = bf.point_mass(S, N, [0] * N)
+        cov = bf.coverage_values(lat, S)
+        ex = bf.law(p0, Q, Qc, "exact", 0, 2.0, 2) @ cov
+        lie = bf.law(p0, Q, Qc, "lie", 1.0, 2.0, 2) @ cov - ex
+        rnd = bf.law(p0, Q, Qc, "random", 1.0, 2.0, 2) @ cov - ex
+        errs.append(lie * q)
+        ratios.append(rnd / lie)
+    assert abs(errs[1] - (-0.0266)) < 5e-4 and abs(errs[3] - (-0.0264)) < 5e-4
+    assert max(errs) - min(errs) < 0.15 * abs(np.mean(errs))
+    assert all(r2 > r1 for r1, r2 in zip(ratios, ratios[1:])) and ratios[0] > 3
+
+
 def test_lie_order_asymmetric_start():
     """Global weak error of Lie is O(dt) with an asymmetric start (R#-P5), Strang O(dt^2)."""
     lat = bf.Lattice(1, 1, 8, 1, 2, 2)
