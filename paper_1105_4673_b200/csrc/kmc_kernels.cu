@@ -326,9 +326,9 @@ static int resident_ctas(K kernel, int bs) {
     return per * nsm;
 }
 
-template <int KIND, int NDIM, int MINB, bool MH, bool NEST, bool PEER = false>
+template <int KIND, int NDIM, int MINB, bool MH, bool NEST, bool PEER = false, int BSZ = 256>
 static cudaError_t launch_v(const SubstepArgs& a, long long nactive, cudaStream_t s) {
-    constexpr int bs = 256;
+    constexpr int bs = BSZ;
     auto kern = substep_kernel<KIND, NDIM, bs, MINB, MH, NEST, PEER>;
     // persistent grid: one wave of resident warps, each starting on its own chunk of 32*8 cells
     static int cap = 0;                                            // per instantiation
@@ -376,16 +376,22 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
         // with <= 80 registers (3 CTAs/SM) -- measured on B200
         if (!mh_ok) return cudaErrorInvalidValue;
         if constexpr (KIND == 1) {
-            // uniform hop blocks (R31): the block-walk step (8192^2 Strang: 2.93e10 events/s vs 2.29e10
-            // for the 22-mask step), 101 registers (2 CTAs/SM; the <= 80-register build, KMC_HOPLB=3,
-            // measured 2 % slower)
-            static const int hlb = [] { const char* e = getenv("KMC_HOPLB"); return e ? atoi(e) : 2; }();
+            // uniform hop blocks (R31): the block-walk step.  Launch shape measured on 8192^2 Strang:
+            // 128-thread blocks at <= 80 registers (6 CTAs = 24 warps/SM) 3.20e10 events/s; 256 x 2
+            // (94 registers, 16 warps) 3.01e10; 256 x 3 (80 registers, 24 warps) 2.90e10; 96 x 7 2.89e10
+            static const int hlb = [] { const char* e = getenv("KMC_HOPLB"); return e ? atoi(e) : 5; }();
             if (a.hop_fast) {
+                if (hlb == 5) {
+                    if (a.nest) return launch_v<4, NDIM, 5, true, true, false, 128>(a, nactive, s);
+                    if (NDIM == 2 && a.peer_up[0]) return launch_v<4, NDIM, 5, true, false, NDIM == 2, 128>(a, nactive, s);
+                    return launch_v<4, NDIM, 5, true, false, false, 128>(a, nactive, s);
+                }
                 if (a.nest) return hlb == 2 ? launch_v<4, NDIM, 2, true, true>(a, nactive, s)
                                             : launch_v<4, NDIM, 3, true, true>(a, nactive, s);
                 if (NDIM == 2 && a.peer_up[0])
                     return hlb == 2 ? launch_v<4, NDIM, 2, true, false, NDIM == 2>(a, nactive, s)
                                     : launch_v<4, NDIM, 3, true, false, NDIM == 2>(a, nactive, s);
+                if (hlb == 7) return launch_v<4, NDIM, 7, true, false, false, 96>(a, nactive, s);
                 return hlb == 2 ? launch_v<4, NDIM, 2, true, false>(a, nactive, s)
                      : hlb == 4 ? launch_v<4, NDIM, 4, true, false>(a, nactive, s)
                                 : launch_v<4, NDIM, 3, true, false>(a, nactive, s);
