@@ -402,9 +402,10 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
             static const int zf = [] { const char* e = getenv("KMC_ZGBFAST"); return e ? atoi(e) : 1; }();
             if (a.hop_fast && zf) {
                 constexpr int KG = KIND + 3;
-                // <= 64 registers (4 CTAs/SM, 34-byte spill) measured 3 % faster than <= 80 (3 CTAs/SM);
-                // KMC_ZGBLB=3 selects the latter
-                static const int zlb = [] { const char* e = getenv("KMC_ZGBLB"); return e ? atoi(e) : 4; }();
+                // launch shape measured on zgb2d_32768 (after the table-driven member boards): 256 x 3
+                // (<= 80 registers, no spill) 1.98e10 events/s; 256 x 4 (64 registers, 34-byte spill)
+                // 1.91e10; 128 x 6 1.88e10.  KMC_ZGBLB=4 selects the 4-CTA build
+                static const int zlb = [] { const char* e = getenv("KMC_ZGBLB"); return e ? atoi(e) : 3; }();
                 if (zlb == 4 && !a.nest && !a.peer_up[0]) return launch_v<KG, NDIM, 4, true, false>(a, nactive, s);
                 if (a.nest) return launch_v<KG, NDIM, 3, true, true>(a, nactive, s);
                 if (NDIM == 2 && a.peer_up[0]) return launch_v<KG, NDIM, 3, true, false, NDIM == 2>(a, nactive, s);
