@@ -14,10 +14,14 @@
 //        the halo boards, written back once per window with atomicXor of the delta).
 //   No tensor cores: this is not a contraction.  See DESIGN.md §8 for why a lane (not a
 //   warp) owns a cell: the per-event chain is serial, so 32 independent cells per warp
-//   give 32x the issue efficiency of a warp-cooperative scan.  The event step itself is in
-//   kmc_device.cuh (shared with the shared-memory tile kernel of kmc_tile.cu).
-// observables_kernel (a8): integer counts, order-free.
-// pack / unpack: uint8 site-major <-> bit-packed cell-major.
+//   give 32x the issue efficiency of a warp-cooperative scan.  The event steps are in
+//   kmc_device.cuh: event_step (generic, every model; also used by the tile kernel of
+//   kmc_tile.cu), event_step_hop (diffusion, n-major hop blocks, R31; KIND 4) and
+//   event_step_zgb_grouped (ZGB with one rate per direction group; KINDs 5, 6).
+// observables_kernel (a8): integer counts, order-free, one launch per observation.
+// correlation_kernel, series_*_kernel (f1): pair counts; the coverage process and its statistics.
+// strip / cdf kernels (f4), init_random_kernel (R32), pack / unpack (uint8 site-major <->
+// bit-packed cell-major), exchange helpers (flags, XOR rows) for the multi-GPU slabs.
 #include "kmc_device.cuh"
 
 #include <cassert>
