@@ -792,3 +792,29 @@ def test_fused_exchange_bit_identical(kind, params, cell, scheme, dt, world):
     assert a["events"] == b["events"] > 0
     for key in ("n_state", "nn_pairs", "n_state_by_colour"):
         assert np.array_equal(a[key], b[key]), key
+
+
+def test_maximum_size_lattice():
+    """A 65536^2 lattice (4.3e9 sites, 2^26 cells: 32-bit word and cell ids near their range) runs a
+    Lie macro-step: the observables count every site, events happen, two contexts with the same seed
+    and configuration give identical lattices (no index overflow, no races), and a replica offset
+    beyond 2^31 cells is refused (kmc_create keeps every id below 2^32)."""
+    torch = _cuda()
+    import paper_1105_4673_b200 as kmc
+    n = 65536
+    p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)
+    outs = []
+    for _ in range(2):
+        g = kmc.KMC(2, (n, n), (8, 8), kind="adsdes", seed=5, **p)
+        g.init_random((0.5, 0.5), seed=9)
+        g.run(1.0, 1.0, "lie")
+        o = g.observables()
+        assert int(o["n_state"][0] + o["n_state"][1]) == n * n
+        assert o["events"] > 1.0 * n * n
+        w = torch.from_numpy(g.get_config_packed().view(np.int64)).cuda()
+        outs.append((int(w.sum().item()), int((w * 3 + 1).sum().item()), int(w[::7].sum().item())))
+        del g, w
+        torch.cuda.empty_cache()
+    assert outs[0] == outs[1]
+    with pytest.raises(kmc.KmcError):
+        kmc.KMC(2, (n, n), (8, 8), kind="adsdes", replicas=65, seed=5, **p)   # 65 x 2^26 cells > 2^32
