@@ -381,8 +381,8 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
         if (!mh_ok) return cudaErrorInvalidValue;
         if constexpr (KIND == 1) {
             // uniform hop blocks (R31): the block-walk step.  Launch shape measured on 8192^2 Strang:
-            // 128-thread blocks at <= 80 registers (6 CTAs = 24 warps/SM) 3.20e10 events/s; 256 x 2
-            // (94 registers, 16 warps) 3.01e10; 256 x 3 (80 registers, 24 warps) 2.90e10; 96 x 7 2.89e10
+            // 128-thread blocks (88 registers, 5 CTAs = 20 warps/SM) 3.20e10 events/s; 256 x 2 (94
+            // registers, 16 warps) 3.01e10; 256 x 3 (80 registers, 24 warps) 2.90e10; 96 x 7 2.89e10
             static const int hlb = [] { const char* e = getenv("KMC_HOPLB"); return e ? atoi(e) : 5; }();
             if (a.hop_fast) {
                 if (hlb == 5) {
