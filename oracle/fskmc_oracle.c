@@ -355,9 +355,14 @@ int64_t orc_window(uint8_t* lat, int R, int64_t H, int64_t W, int ndim, int qx, 
     const double inv_scale = ldexp(1.0, -F);          /* 2^-F */
     const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     int64_t total = 0;
-    for (int64_t rep = 0; rep < R; ++rep)
-    for (int64_t cy = 0; cy < My; ++cy)
-    for (int64_t cx = 0; cx < Mx; ++cx) {
+    /* The cells of one colour are independent within a window (eq.(exact); same-colour
+     * closures are disjoint, R6), so the timing build (tools/oracle_timing.py, -fopenmp) runs them
+     * on all host cores with identical results; the test build is single-threaded. */
+#ifdef _OPENMP
+#pragma omp parallel for reduction(+ : total) schedule(dynamic, 64)
+#endif
+    for (int64_t t = 0; t < (int64_t)R * My * Mx; ++t) {
+        const int64_t rep = t / (My * Mx), cy = (t / Mx) % My, cx = t % Mx;
         if (orc_cell_colour(ndim, C, cy, cx) != colour) continue;
         const uint64_t gid = (uint64_t)rep * (uint64_t)(Mx * My) + (uint64_t)(cy * Mx + cx);
         uint32_t k = cell_window(&L, rep, cy, cx, qx, qy, gid, D, window, key,
