@@ -76,5 +76,5 @@ def philox4x32_10(ctr, key):
 
 
 def log_spec(x: float) -> float:
-    """The specified natural log (fdlibm e_log.c operation sequence), DESIGN.md §3."""
+    """The specified natural log: the table-driven FMA sequence of DESIGN.md §3.1 (reading R26)."""
     return lib().orc_log(float(x))
