@@ -132,7 +132,7 @@ def l2_policy(wl, dims_per_gpu):
                   f"bit-packed lattice {nbytes / 2**20:.3g} MiB/GPU)")
 
 
-def arm_config(workload, dt, world, fused=False, scaling="weak"):
+def arm_config(workload, dt, world, fused=False, scaling="weak", loopback=False):
     """The `config` object of both arms (the workload the metric is quoted on)."""
     wl = si.WORKLOADS[workload]
     C = 2 if (wl["ndim"] == 1 or wl["kind"] == "adsdes") else 4
@@ -147,8 +147,9 @@ def arm_config(workload, dt, world, fused=False, scaling="weak"):
             "replicas_per_gpu": wl.get("replicas_per_gpu", 1),
             "l2": l2_policy(wl, per_gpu)[1],
             "parallelism": (f"slab{world}" if wl["ndim"] == 2 else f"replicas{world}"),
-            "exchange": ("fused (peer writes in the window kernel)" if fused else "nccl send/recv")
-                        if wl["ndim"] == 2 and world > 1 else "none"}
+            "exchange": ((("fused (peer writes in the window kernel)" if fused else "nccl send/recv")
+                         + (" to itself (one-rank ring, NCCL loopback)" if loopback and world == 1 else ""))
+                        if wl["ndim"] == 2 and (world > 1 or loopback) else "none")}
 
 
 def run_reference(args):
@@ -195,7 +196,18 @@ def main():
                     help="weak: one workload-sized slab per GPU (default); strong: the workload split over the GPUs")
     ap.add_argument("--fused-exchange", action="store_true",
                     help="N > 1: halo exchange folded into the window kernel (CUDA IPC + device flags)")
+    ap.add_argument("--loopback", action="store_true",
+                    help="N = 1, 2D: run the lattice as a one-rank ring through the multi-GPU data plane "
+                         "(NCCL send/recv to itself, or the fused exchange) to measure its cost on one GPU")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver's own N > 1 launch
+        # sets WORLD_SIZE and lands below directly)
+        import random
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(random.randint(20000, 40000)),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -207,8 +219,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     uid = None
+    if world == 1 and args.loopback:
+        uid = kmc.nccl_unique_id()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         box = [kmc.nccl_unique_id() if rank == 0 else None]
@@ -232,7 +248,7 @@ def main():
     torch.cuda.set_stream(stream)
     k = kmc.KMC(ndim, gdims, wl["cell"], kind=wl["kind"], replicas=wl.get("replicas_per_gpu", 1) * (world if ndim == 1 else 1),
                 seed=0xB200, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=uid,
-                fused_exchange=args.fused_exchange and world > 1, **wl["params"])
+                fused_exchange=args.fused_exchange and (world > 1 or args.loopback), **wl["params"])
     shape = k.local_shape
     if wl["kind"].startswith("zgb"):
         lat = si.categorical_lattice(shape, [1.0 - wl["init"], wl["init"] / 2, wl["init"] / 2] if wl["init"] else [1.0, 0.0, 0.0],
@@ -397,7 +413,7 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64",
         "data": "synthetic",
-        "config": arm_config(args.workload, dt, world, args.fused_exchange, args.scaling),
+        "config": arm_config(args.workload, dt, world, args.fused_exchange, args.scaling, args.loopback),
         "site_updates_per_s": site_updates,
         "events_per_step": events / args.steps,
         "roofline": roof,

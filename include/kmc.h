@@ -61,13 +61,16 @@ typedef enum { KMC_LIE = 0, KMC_STRANG = 1, KMC_RANDOM = 2 } kmc_scheme;
  *  ZGB          Table COrates P:1132-1148 (R13): [CO adsorb k1] [O2 adsorb (1-k1)/z per
  *               vacant neighbour d] [CO+O react k2/z, CO anchor, d] [CO+O react k2/z, O anchor, d]
  *  ZGB_DIFF     + CO hops c_hop per vacant neighbour d
+ *  ZGB_ODIFF    + O hops c_hop per vacant neighbour d: the fast O-adsorbate diffusion the paper's ZGB
+ *               runs omit and its Strang scheme is meant to add (R33) -- the fast
+ *               mechanism of kmc_run_multiscale by default
  *  z = 2 ndim.  */
-typedef enum { KMC_ADSDES = 0, KMC_ADSDES_DIFF = 1, KMC_ZGB = 2, KMC_ZGB_DIFF = 3 } kmc_model_kind;
+typedef enum { KMC_ADSDES = 0, KMC_ADSDES_DIFF = 1, KMC_ZGB = 2, KMC_ZGB_DIFF = 3, KMC_ZGB_ODIFF = 4 } kmc_model_kind;
 
 typedef struct {
     int32_t kind;                 /* kmc_model_kind */
     double ca, cd, beta, K, h;    /* Arrhenius ads/des (c1 = ca, c2 = cd) */
-    double c_hop;                 /* hop prefactor (R12; ZGB_DIFF: CO hop rate) */
+    double c_hop;                 /* hop prefactor (R12; ZGB_DIFF: CO hop rate; ZGB_ODIFF: O hop rate) */
     double k1, k2;                /* ZGB (R14) */
 } kmc_model;
 
@@ -83,13 +86,18 @@ typedef struct {
 typedef struct {
     int32_t rank, world;          /* world = 1: single GPU.  world > 1: 2D slabs along y, 1D replicas split */
     int32_t device;               /* CUDA device ordinal */
-    const uint8_t* nccl_unique_id;/* 128 bytes from kmc_nccl_unique_id() on rank 0, broadcast; NULL if world = 1 */
+    const uint8_t* nccl_unique_id;/* 128 bytes from kmc_nccl_unique_id() on rank 0, broadcast.  world = 1: NULL,
+                                     or -- 2D only -- an id to run the lattice as a ONE-RANK PERIODIC RING
+                                     through the multi-GPU data plane (NCCL loopback): ghost rows, the
+                                     NCCL send/recv exchange with itself (and with fused_exchange = 1 the
+                                     peer-write kernel variant and device flags on its own planes), so
+                                     that transport executes on a single GPU; bit-identical to NULL */
     void* stream;                 /* cudaStream_t to launch on (e.g. torch's current stream); NULL = library-owned */
     const int64_t* row_bounds;    /* 2D, world > 1: world+1 cell-row bounds of the slabs (rank r owns cell rows
                                      [b_r, b_{r+1}), each an even number >= 2; e.g. from
                                      kmc_workload_partition), NULL = the even split.  Results do not depend
                                      on the split (global ids).  KMC_EPARTITION if invalid. */
-    int32_t fused_exchange;       /* 2D, world > 1: 1 = fold the halo exchange into the window kernel (SURVEY
+    int32_t fused_exchange;       /* 2D, world > 1 (or the world = 1 loopback ring): 1 = fold the halo exchange into the window kernel (SURVEY
                                      §8(e)): the neighbours' planes are mapped with CUDA IPC (NVLink peer
                                      memory, one process per GPU on one node), the kernel writes the shared
                                      rows directly and windows are ordered by device-side flags instead of
@@ -136,8 +144,13 @@ kmc_status kmc_local_shape(const kmc_ctx* ctx, int64_t* replicas_local, int64_t*
 kmc_status kmc_init_random(kmc_ctx* ctx, const double* probs, int32_t nprobs, uint64_t seed);
 kmc_status kmc_set_config(kmc_ctx* ctx, const uint8_t* host_local_slab, int64_t nbytes);
 kmc_status kmc_get_config(kmc_ctx* ctx, uint8_t* host_local_slab, int64_t nbytes);
-/* Same with a device buffer (e.g. a torch CUDA tensor), stream-ordered, no validation report
- * (out-of-range spins are clamped to vacant and counted; see kmc_observables). */
+/* Same with a device buffer (e.g. a torch CUDA tensor), stream-ordered and asynchronous, so no
+ * validation status: out-of-range spins are clamped to vacant and flagged; kmc_device_errors reports
+ * whether the last kmc_set_config_device had any.  The lattice stays in the library's bit-packed
+ * device planes (8x smaller than the uint8 buffer): the caller's buffer is read (set)
+ * or written (get) during the call's stream work only and is never borrowed -- the uint8 site-major
+ * layout of §8(b)'s borrowed kmc_dist.lattice cannot be the working layout of the bit-board kernels,
+ * so kmc_dist has no such field; kmc_set/get_config_packed move the working layout itself. */
 kmc_status kmc_set_config_device(kmc_ctx* ctx, const uint8_t* dev_local_slab, int64_t nbytes);
 kmc_status kmc_get_config_device(kmc_ctx* ctx, uint8_t* dev_local_slab, int64_t nbytes);
 /* Bit-packed local slab (host buffers; the checkpoint format and the cheap upload path -- 1 bit per
@@ -173,7 +186,8 @@ kmc_status kmc_run(kmc_ctx* ctx, double T, double dt, kmc_scheme scheme);
  *   e^{d/2 L_slow} [ e^{(d/n_fast) L_fast} ]^{n_fast} e^{d/2 L_slow},
  * every factor itself split over the colours with the `inner` scheme (Lie, Strang or random, as in
  * kmc_run) -- the spatio-temporal hierarchy of P:750-753.  fast_classes: bit i = class i of the rate
- * table is fast (0 = the hop classes, e.g. ZGB_DIFF's CO diffusion).  Windows of one
+ * table is fast (0 = the hop classes: ADSDES_DIFF's hops, ZGB_DIFF's CO or ZGB_ODIFF's O diffusion,
+ * P:1211-1213).  Windows of one
  * mechanism run with the other mechanism's rates set to 0.  KMC_EINVAL when the fast set is empty or
  * covers every class; KMC_WTRUNCATED as kmc_run.  Asynchronous. */
 kmc_status kmc_run_multiscale(kmc_ctx* ctx, double T, double dt, int32_t n_fast, kmc_scheme inner,
@@ -212,6 +226,12 @@ kmc_status kmc_observables(kmc_ctx* ctx, kmc_obs* out, uint32_t* per_cell_events
  * (what kmc_observables returns for the same state). */
 #define KMC_OBS_WORDS 40
 kmc_status kmc_observables_device(kmc_ctx* ctx, uint64_t* dev_counters);
+/* Device-side error words (synchronises the context's stream): *bad_spins = 1 if the last
+ * kmc_set_config_device held spin values >= the number of states (clamped to vacant);
+ * *wait_timeouts = 1 if a fused-exchange flag wait gave up after 60 s (a neighbour rank never
+ * arrived; the windows after it ran unordered and the state is void -- kmc_observables then returns
+ * KMC_ECUDA).  Either pointer may be NULL. */
+kmc_status kmc_device_errors(kmc_ctx* ctx, int32_t* bad_spins, int32_t* wait_timeouts);
 kmc_status kmc_obs_decode(const kmc_ctx* ctx, const uint64_t* counters, kmc_obs* out);
 
 /* Two-point correlation counts (the paper's 2-point correlation function
@@ -302,6 +322,9 @@ kmc_status kmc_vgroup_sync(kmc_ctx** ctxs, int32_t world);
  * bit-identical to the exchange protocol and to world = 1.  Nested runs keep the exchange path.
  * While enabled, configuration uploads copy into the planes instead of swapping buffers. */
 kmc_status kmc_vgroup_set_fused(kmc_ctx** ctxs, int32_t world, int32_t enable);
+/* kmc_observables of the whole virtual-rank group (ghost rows refreshed first): the integer counters
+ * and events summed over the ranks, coverage and energy (R24) decoded from the sums.  Synchronous. */
+kmc_status kmc_vgroup_observables(kmc_ctx** ctxs, int32_t world, kmc_obs* out);
 /* kmc_run_nested on a virtual-rank group (one exchange per outer factor). */
 kmc_status kmc_vgroup_run_nested(kmc_ctx** ctxs, int32_t world, double T, double dt, int32_t n_inner,
                                  kmc_scheme outer, kmc_scheme inner, int32_t block);

@@ -79,12 +79,15 @@ def _events(model, lat, conf, i):
             for j in nb:
                 if conf[j] == 1:
                     ev.append((k2 / z, {i: 0, j: 0}))
+                if kind == "zgb_odiff" and conf[j] == 0:     # fast O diffusion
+                    ev.append((model["c_hop"], {i: 0, j: 2}))
     return ev
 
 
-def _is_hop(i, upd):
-    """Diffusion events move a particle: the anchor empties and one neighbour fills (state 1)."""
-    return len(upd) == 2 and upd[i] == 0 and any(j != i and v == 1 for j, v in upd.items())
+def _is_hop(i, upd, conf):
+    """Diffusion events move a particle: the anchor empties and one neighbour takes its species."""
+    return (len(upd) == 2 and upd[i] == 0 and conf[i] != 0
+            and any(j != i and v == conf[i] for j, v in upd.items()))
 
 
 def generators(model, lat, mech=None):
@@ -104,7 +107,7 @@ def generators(model, lat, mech=None):
             for rate, upd in _events(model, lat, conf, i):
                 if rate == 0.0:
                     continue
-                if mech is not None and (mech == "fast") != _is_hop(i, upd):
+                if mech is not None and (mech == "fast") != _is_hop(i, upd, conf):
                     continue
                 to = idx + sum((v - conf[j]) * powers[j] for j, v in upd.items())
                 rows[c].append(idx); cols[c].append(to); vals[c].append(rate)

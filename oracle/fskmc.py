@@ -22,8 +22,8 @@ import numpy as np
 
 from . import lib, philox4x32_10
 
-KIND = {"adsdes": 0, "adsdes_diff": 1, "zgb": 2, "zgb_diff": 3}
-NSTATES = {0: 2, 1: 2, 2: 3, 3: 3}
+KIND = {"adsdes": 0, "adsdes_diff": 1, "zgb": 2, "zgb_diff": 3, "zgb_odiff": 4}
+NSTATES = {0: 2, 1: 2, 2: 3, 3: 3, 4: 3}
 LIE, STRANG, RANDOM = 0, 1, 2
 SCHEME = {"lie": LIE, "strang": STRANG, "random": RANDOM}
 TAG_SCHED = 1
@@ -225,11 +225,11 @@ class FSKMC:
     def run_multiscale(self, T: float, dt: float, n_fast: int, inner="lie", fast_classes=None) -> bool:
         """f2, eq.(strang3): per macro-step d, e^{d/2 L_slow} [e^{(d/n) L_fast}]^n
         e^{d/2 L_slow}, each factor split over the colours with the `inner` scheme.
-        Fast classes default to the hop slot types (R12 diffusion / ZGB CO diffusion)."""
+        Fast classes default to the hop slot types (R12 diffusion / ZGB CO or O diffusion)."""
         sc = SCHEME[inner] if isinstance(inner, str) else int(inner)
         n = self.table["n"]
         if fast_classes is None:
-            fast = {i for i in range(n) if int(self.table["type"][i]) in (2, 7)}   # T_HOP, T_COHOP
+            fast = {i for i in range(n) if int(self.table["type"][i]) in (2, 7, 8)}   # T_HOP, T_COHOP, T_OHOP
         else:
             fast = set(fast_classes)
         slow = set(range(n)) - fast

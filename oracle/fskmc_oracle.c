@@ -118,8 +118,8 @@ double orc_log(double x)
 /* ------------------------------------------------------------------ */
 /* Models, slot types and the canonical class list.   */
 /* ------------------------------------------------------------------ */
-enum { M_ADSDES = 0, M_ADSDES_DIFF = 1, M_ZGB = 2, M_ZGB_DIFF = 3 };
-enum { T_ADS = 0, T_DES = 1, T_HOP = 2, T_COADS = 3, T_O2ADS = 4, T_RCO = 5, T_RO = 6, T_COHOP = 7 };
+enum { M_ADSDES = 0, M_ADSDES_DIFF = 1, M_ZGB = 2, M_ZGB_DIFF = 3, M_ZGB_ODIFF = 4 };
+enum { T_ADS = 0, T_DES = 1, T_HOP = 2, T_COADS = 3, T_O2ADS = 4, T_RCO = 5, T_RO = 6, T_COHOP = 7, T_OHOP = 8 };
 #define MAXCLASS 32
 
 /* params[] = {ca, cd, beta, K, h, c_hop, k1, k2} */
@@ -153,7 +153,7 @@ int orc_classes(int kind, int ndim, const double* params,
         }
         return n;
     }
-    if (kind == M_ZGB || kind == M_ZGB_DIFF) {
+    if (kind == M_ZGB || kind == M_ZGB_DIFF || kind == M_ZGB_ODIFF) {
         /* Table COrates, storage 0 vacant, 1 CO, 2 O (R13); one slot per direction (R13) */
         ctype[n] = T_COADS; cdir[n] = -1; ckappa[n] = 0; crate[n] = k1; ++n;
         for (int d = 0; d < z; ++d) { ctype[n] = T_O2ADS; cdir[n] = d; ckappa[n] = 0; crate[n] = (1.0 - k1) / (double)z; ++n; }
@@ -161,6 +161,10 @@ int orc_classes(int kind, int ndim, const double* params,
         for (int d = 0; d < z; ++d) { ctype[n] = T_RO;    cdir[n] = d; ckappa[n] = 0; crate[n] = k2 / (double)z; ++n; }
         if (kind == M_ZGB_DIFF)
             for (int d = 0; d < z; ++d) { ctype[n] = T_COHOP; cdir[n] = d; ckappa[n] = 0; crate[n] = chop; ++n; }
+        /* the fast O-adsorbate diffusion the paper leaves out of ZGB (after \cite{evans09}):
+         * O(x), vacant y = x + e_d -> vacant, O at c_hop per vacant neighbour direction (R33) */
+        if (kind == M_ZGB_ODIFF)
+            for (int d = 0; d < z; ++d) { ctype[n] = T_OHOP; cdir[n] = d; ckappa[n] = 0; crate[n] = chop; ++n; }
         return n;
     }
     return -1;
@@ -175,6 +179,7 @@ int orc_types_per_site(int kind, int ndim)
     case M_ADSDES_DIFF: return 2 + z;
     case M_ZGB: return 1 + 3 * z;
     case M_ZGB_DIFF: return 1 + 4 * z;
+    case M_ZGB_ODIFF: return 1 + 4 * z;
     }
     return -1;
 }
@@ -249,6 +254,7 @@ static int slot_kappa(const latview* L, int64_t rep, int64_t y, int64_t x, int t
     case T_RCO: return s == 1 && p == 2;
     case T_RO: return s == 2 && p == 1;
     case T_COHOP: return s == 1 && p == 0;
+    case T_OHOP: return s == 2 && p == 0;
     }
     return 0;
 }
@@ -266,6 +272,7 @@ static void apply_slot(latview* L, int64_t rep, int64_t y, int64_t x, int type, 
     case T_RCO:   set_site(L, rep, y, x, 0); set_site(L, rep, py, px, 0); break;
     case T_RO:    set_site(L, rep, y, x, 0); set_site(L, rep, py, px, 0); break;
     case T_COHOP: set_site(L, rep, y, x, 0); set_site(L, rep, py, px, 1); break;
+    case T_OHOP:  set_site(L, rep, y, x, 0); set_site(L, rep, py, px, 2); break;
     }
 }
 

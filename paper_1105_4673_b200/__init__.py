@@ -19,8 +19,8 @@ LIB_PATH = os.environ.get("KMC_B200_LIB", LIB_PATH)
 KMC_OK, KMC_EINVAL, KMC_EPARTITION, KMC_ENOMEM, KMC_ECUDA, KMC_ENCCL, KMC_ESTATE = 0, 1, 2, 3, 4, 5, 6
 KMC_WTRUNCATED = 100
 SCHEMES = {"lie": 0, "strang": 1, "random": 2}
-KINDS = {"adsdes": 0, "adsdes_diff": 1, "zgb": 2, "zgb_diff": 3}
-NSTATES = {0: 2, 1: 2, 2: 3, 3: 3}
+KINDS = {"adsdes": 0, "adsdes_diff": 1, "zgb": 2, "zgb_diff": 3, "zgb_odiff": 4}
+NSTATES = {0: 2, 1: 2, 2: 3, 3: 3, 4: 3}
 
 # Every symbol include/kmc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -34,7 +34,7 @@ EXPORTS = [
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
     "kmc_vgroup_set_fused", "kmc_abi_sizes", "kmc_record_coverage", "kmc_coverage_series", "kmc_coverage_stats",
     "kmc_stage_config_packed", "kmc_commit_config", "kmc_observables_device", "kmc_obs_decode",
-    "kmc_init_random",
+    "kmc_init_random", "kmc_device_errors", "kmc_vgroup_observables",
 ]
 OBS_WORDS = 40
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
@@ -128,6 +128,8 @@ def lib():
         "kmc_commit_config": ([vp], i32),
         "kmc_coverage_series": ([vp, vp, i64, P(i64)], i32),
         "kmc_coverage_stats": ([vp, i64, i32, vp, vp, i32, vp], i32),
+        "kmc_device_errors": ([vp, P(i32), P(i32)], i32),
+        "kmc_vgroup_observables": ([vp, i32, P(KmcObs)], i32),
     }
     ab_build = "KMC_B200_LIB" in os.environ          # an older build under comparison may lack new entry points
     for name, (args, res) in sig.items():
@@ -398,6 +400,13 @@ class KMC:
                                                int(bins), hist.ctypes.data if bins else None))
         return {"mean": float(mom[0]), "var": float(mom[1]), "acf": acf, "hist": hist}
 
+    def device_errors(self):
+        """kmc_device_errors: {'bad_spins': last set_config_device clamped out-of-range spins,
+        'wait_timeouts': a fused-exchange flag wait gave up} (synchronises)."""
+        b, t = ctypes.c_int32(), ctypes.c_int32()
+        self._check(self._L.kmc_device_errors(self._ctx, ctypes.byref(b), ctypes.byref(t)))
+        return {"bad_spins": bool(b.value), "wait_timeouts": bool(t.value)}
+
     def get_state(self):
         w, t = ctypes.c_uint64(), ctypes.c_double()
         self._check(self._L.kmc_get_state(self._ctx, ctypes.byref(w), ctypes.byref(t)))
@@ -520,17 +529,10 @@ class VGroup:
         return _partition(self._L, self._check, fn, self._arr, parts, granule, self._strips)
 
     def observables(self):
-        """Group sum of the integer counters (ghost rows refreshed first)."""
-        self._check(self._L.kmc_vgroup_sync(self._arr, self.world))
-        obs = [rk.observables() for rk in self.ranks]
-        out = dict(obs[0])
-        for key in ("n_state", "nn_pairs", "n_state_by_colour"):
-            out[key] = sum(o[key] for o in obs)
-        out["events"] = sum(o["events"] for o in obs)
-        n = out["n_state"].sum()
-        out["coverage"] = out["n_state"] / n
-        out["energy"] = -self.model.K * float(out["nn_pairs"][1, 1]) + self.model.h * float(out["n_state"][1])
-        return out
+        """kmc_vgroup_observables: the group's observables (counters summed over the ranks in C)."""
+        o = KmcObs()
+        self._check(self._L.kmc_vgroup_observables(self._arr, self.world, ctypes.byref(o)))
+        return KMC._obs_dict(o)
 
     def close(self):
         for rk in self.ranks:

@@ -164,6 +164,7 @@ struct kmc_ctx {
     // multi-GPU
     ncclComm_t comm = nullptr;
     int rank_up = -1, rank_down = -1;        // -y and +y ring neighbours (2D slabs)
+    std::vector<int64_t> bounds;             // 2D: cell-row bounds of every rank's slab (world + 1)
     std::string err;
 };
 
@@ -190,6 +191,7 @@ int types_per_site(int kind, int z) {
     case KMC_ADSDES_DIFF: return 2 + z;
     case KMC_ZGB: return 1 + 3 * z;
     case KMC_ZGB_DIFF: return 1 + 4 * z;
+    case KMC_ZGB_ODIFF: return 1 + 4 * z;
     }
     return 0;
 }
@@ -224,6 +226,8 @@ int build_classes(const kmc_model& m, int ndim, int* type, int* dir, int* kappa,
     for (int d = 0; d < z; ++d) add(T_RO, d, 0, m.k2 / (double)z);
     if (m.kind == KMC_ZGB_DIFF)
         for (int d = 0; d < z; ++d) add(T_COHOP, d, 0, m.c_hop);
+    if (m.kind == KMC_ZGB_ODIFF)   // fast O diffusion (R33): O(x), vacant x+e_d -> vacant, O
+        for (int d = 0; d < z; ++d) add(T_OHOP, d, 0, m.c_hop);
     return n;
 }
 
@@ -258,8 +262,12 @@ long long active_cells(const kmc_ctx* c) {
 // a7 forward exchange (world > 1, 2D): owned boundary cell rows -> neighbours' ghost rows.
 // f1 (R30): append one sample of the coverage process (per-replica count of series_state over the
 // owned cells) to the device series; stream-ordered, no host synchronisation.  Full: no-op.
+kmc_status fused_quiesce(kmc_ctx* c);
+
 kmc_status record_sample(kmc_ctx* c) {
     if (!c->series || c->series_n >= c->series_cap) return KMC_OK;
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     unsigned long long* out = c->series + (size_t)c->series_n * c->g.R;
     CUDA_TRY(c, cudaMemsetAsync(out, 0, (size_t)c->g.R * 8, c->stream));
     SeriesArgs a{};
@@ -275,7 +283,7 @@ kmc_status record_sample(kmc_ctx* c) {
 }
 
 kmc_status exchange_forward(kmc_ctx* c) {
-    if (c->world == 1 || c->g.ndim == 1 || !c->comm) return KMC_OK;   // vgroup: exchanged by its driver
+    if (!c->comm || !c->g.ghost) return KMC_OK;   // world 1 (no ring), 1D, vgroup (exchanged by its driver)
     const size_t rowlen = (size_t)c->g.R * c->g.Mx;
     const int My = c->g.My_local;
     NCCL_TRY(c, g_nccl.GroupStart());
@@ -302,7 +310,7 @@ kmc_status exchange_forward(kmc_ctx* c) {
 // a7 reverse exchange for cross-cell-writing models: ghost-row deltas back to their owners,
 // merged by XOR (same-colour closures are disjoint, R6, so exactly one writer per bit).
 kmc_status exchange_reverse(kmc_ctx* c) {
-    if (c->world == 1 || c->g.ndim == 1 || !c->cross || !c->comm) return KMC_OK;
+    if (!c->comm || !c->g.ghost || !c->cross) return KMC_OK;
     const size_t rowlen = (size_t)c->g.R * c->g.Mx;
     const int My = c->g.My_local;
     for (int p = 0; p < c->nplanes; ++p) {   // snap := ghost XOR snap  (the delta)
@@ -408,9 +416,9 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     // rate_per_cell: mu >= 16 (Ising dt = 1, diffusion): spin flip 3, diffusion 4; mu < 16
     // (Ising dt = 0.01, ZGB dt = 0.1): spin flip 10, ZGB 16 (+8 % over 8).  Env KMC_REFILL overrides.
     static const int refill_env = [] { const char* e = getenv("KMC_REFILL"); return e ? atoi(e) : 0; }();
-    static const int refill_hi[4] = {3, 4, 6, 6}, refill_lo[4] = {10, 10, 16, 16};
+    static const int refill_hi[5] = {3, 4, 6, 6, 6}, refill_lo[5] = {10, 10, 16, 16, 16};   // by model kind
     a.refill_min = refill_env >= 1 && refill_env <= 32 ? refill_env
-                 : (D * c->rate_per_cell >= 16.0 ? refill_hi[c->kind & 3] : refill_lo[c->kind & 3]);
+                 : (D * c->rate_per_cell >= 16.0 ? refill_hi[c->kind] : refill_lo[c->kind]);
     a.w_lo = (uint32_t)c->window;
     a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
     if (class_mask != ~0ull)
@@ -425,7 +433,7 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
         }
         static const int hop_env = [] { const char* e = getenv("KMC_HOPFAST"); return e ? atoi(e) : 1; }();
         if (!hop_env) a.hop_fast = 0;
-    } else if (c->kind == KMC_ZGB || c->kind == KMC_ZGB_DIFF) {   // one rate per direction group
+    } else if (c->kind >= KMC_ZGB) {   // ZGB*: one rate per direction group
         const int z = 2 * c->g.ndim;
         a.hop_fast = 1;
         for (int i = 1; i < c->nclass; ++i)
@@ -462,11 +470,22 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     return KMC_OK;
 }
 
-// Fused exchange across GPUs: the ghost rows are refreshed by one NCCL exchange at the start of every
-// call that runs windows (configuration uploads may have changed the neighbours' rows); afterwards
-// the window kernels keep them current.  Every rank makes the same calls, so this stays collective.
+// Fused exchange across GPUs: the neighbours' windows write into this rank's boundary and ghost rows
+// through peer memory, so ANY other use of the planes (exchange, upload, download, observables,
+// coverage samples, random init) is first ordered after both neighbours' last window: a one-thread
+// wait kernel on the device flags, stream-ordered (no host synchronisation).
+kmc_status fused_quiesce(kmc_ctx* c) {
+    if (c->fused_ipc) CUDA_TRY(c, launch_wait_flags(c->flags, c->epoch, c->stream));
+    return KMC_OK;
+}
+
+// ... and the ghost rows are refreshed by one NCCL exchange at the start of every call that runs
+// windows (configuration uploads may have changed the neighbours' rows); afterwards the window
+// kernels keep them current.  Every rank makes the same calls, so this stays collective.
 kmc_status fused_refresh(kmc_ctx* c) {
-    return c->fused_ipc ? exchange_forward(c) : KMC_OK;
+    if (!c->fused_ipc) return KMC_OK;
+    kmc_status st = fused_quiesce(c);
+    return st != KMC_OK ? st : exchange_forward(c);
 }
 
 kmc_status do_substep(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull) {
@@ -535,12 +554,18 @@ kmc_status check_nested(kmc_ctx* c, double T, double dt, int n_inner, int outer,
     if (c->g.ndim == 1) {
         if (c->g.Mx % (2 * block)) return fail(c, KMC_EPARTITION, "nested: %d cells not a multiple of 2*block", c->g.Mx);
     } else {
-        const long long rows = (long long)c->g.My_local * c->world;
+        // the GLOBAL cell-row count (uneven slabs: not My_local x world), so every rank agrees
+        const long long rows = c->geom.dims[0] / c->g.qy;
         if (rows % (2 * block)) return fail(c, KMC_EPARTITION, "nested: %lld cell rows not a multiple of 2*block", rows);
         // outer blocks must not straddle ranks: then a rank's ghost rows belong to the other outer
-        // colour for a whole outer factor, and one exchange per outer factor suffices
-        if (c->world > 1 && c->g.My_local % block)
-            return fail(c, KMC_EPARTITION, "nested: %d local cell rows not a multiple of block", c->g.My_local);
+        // colour for a whole outer factor, and one exchange per outer factor suffices.  Checked on
+        // EVERY slab bound (all ranks hold the same bounds), so no rank enters the collective
+        // exchange while another one fails here.
+        if (c->world > 1)
+            for (size_t r = 0; r < c->bounds.size(); ++r)
+                if (c->bounds[r] % block)
+                    return fail(c, KMC_EPARTITION, "nested: slab bound %lld (cell rows) not a multiple of block",
+                                (long long)c->bounds[r]);
     }
     return KMC_OK;
 }
@@ -669,7 +694,8 @@ static bool setup_fused_ipc(kmc_ctx* c, std::string* why) {
         if (e != cudaSuccess) { *why = std::string(what) + ": " + cudaGetErrorString(e); return false; }
         return true;
     };
-    if (!ck(cudaMalloc((void**)&c->flags, 16), "flags") || !ck(cudaMemset(c->flags, 0, 16), "flags")) return false;
+    // flags: [0] written by the up neighbour, [1] by the down neighbour, [2] wait-timeout flag (own)
+    if (!ck(cudaMalloc((void**)&c->flags, 24), "flags") || !ck(cudaMemset(c->flags, 0, 24), "flags")) return false;
     Blob mine{};
     for (int p = 0; p < c->nplanes; ++p)
         if (!ck(cudaIpcGetMemHandle(&mine.planes[p], c->planes[p]), "cudaIpcGetMemHandle(plane)")) return false;
@@ -693,6 +719,15 @@ static bool setup_fused_ipc(kmc_ctx* c, std::string* why) {
     cudaFree(dsend);
     cudaFree(drecv);
     if (!ok) return false;
+    if (c->rank_up == c->rank) {
+        // NCCL loopback (a one-rank ring): the neighbour is this rank -- its own planes and flags
+        // (CUDA IPC cannot map a handle in the process that exported it); same kernels, same flags
+        for (int p = 0; p < c->nplanes; ++p) c->peer_up[p] = c->peer_dn[p] = c->planes[p];
+        c->peer_up_flags = c->peer_dn_flags = c->flags;
+        c->peer_up_rows = (int)all[(size_t)c->rank].rows;
+        c->fused = c->fused_ipc = true;
+        return true;
+    }
     auto open = [&](const cudaIpcMemHandle_t& hnd, void** ptr) {
         return ck(cudaIpcOpenMemHandle(ptr, hnd, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle") &&
                (c->ipc_open.push_back(*ptr), true);
@@ -720,11 +755,15 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     if (!out) return fail(nullptr, KMC_EINVAL, "NULL out");
     *out = nullptr;
     if (!geom || !model) return fail(nullptr, KMC_EINVAL, "NULL geometry or model");
-    if (model->kind < 0 || model->kind > 3) return fail(nullptr, KMC_EINVAL, "unknown model kind %d", model->kind);
+    if (model->kind < 0 || model->kind > 4) return fail(nullptr, KMC_EINVAL, "unknown model kind %d", model->kind);
     if (geom->ndim != 1 && geom->ndim != 2) return fail(nullptr, KMC_EINVAL, "ndim must be 1 or 2");
     if (geom->replicas < 1) return fail(nullptr, KMC_EINVAL, "replicas must be >= 1");
     const int world = dist ? dist->world : 1, rank = dist ? dist->rank : 0;
     if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, KMC_EINVAL, "bad rank/world");
+    // NCCL loopback (kmc.h, kmc_dist): world = 1 with an NCCL unique id runs a 2D lattice as a
+    // one-rank periodic ring through the multi-GPU data plane -- ghost rows, NCCL send/recv to self
+    // (or the fused exchange with device flags) -- so that transport executes on a single GPU
+    const bool loopback = !vgroup && world == 1 && dist && dist->nccl_unique_id && geom->ndim == 2;
 
     const int ndim = geom->ndim;
     const long long H = ndim == 1 ? 1 : geom->dims[0];
@@ -764,6 +803,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
         kmc_status ps = kmc_partition_plan(geom, model->kind, world, rank, plan);
         if (ps != KMC_OK) return ps;
     }
+    if (loopback) plan[4] = plan[5] = 0;                     // a ring of one: both neighbours are rank 0
 
     kmc_ctx* c = new kmc_ctx();
     c->geom = *geom;
@@ -782,7 +822,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     g.rep_offset = (int)plan[0];
     g.row_offset = (int)plan[2];
     g.My_local = (int)plan[3];
-    g.ghost = (world > 1 && ndim == 2) ? 1 : 0;
+    g.ghost = ((world > 1 || loopback) && ndim == 2) ? 1 : 0;
     g.M_global = Mx * My;
     g.shN = qx * (qy - 1);
     g.valid = lowmask(qx * qy);
@@ -797,6 +837,11 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     c->H_local = (long long)g.My_local * qy;
     c->rank_up = (int)plan[4];
     c->rank_down = (int)plan[5];
+    if (ndim == 2) {   // every rank's slab bounds (the same on every rank: collective checks, f3)
+        c->bounds.resize((size_t)world + 1);
+        for (int r = 0; r <= world; ++r)
+            c->bounds[(size_t)r] = (dist && dist->row_bounds && world > 1) ? dist->row_bounds[r] : (int64_t)r * (My / world);
+    }
 
     // a1: the rate table
     c->nclass = build_classes(*model, ndim, c->ctype, c->cdir, c->ckappa, c->crate);
@@ -855,7 +900,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
 
     c->vgroup = vgroup;
     build_args_template(c);
-    if (world > 1 && !vgroup) {
+    if ((world > 1 || loopback) && !vgroup) {
         std::string why;
         if (!dist->nccl_unique_id) { kmc_destroy(c); return fail(nullptr, KMC_EINVAL, "world > 1 needs nccl_unique_id"); }
         if (!load_nccl(&why)) { kmc_destroy(c); return fail(nullptr, KMC_ENCCL, "%s", why.c_str()); }
@@ -863,7 +908,7 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
         memcpy(&id, dist->nccl_unique_id, 128);
         ncclResult_t r = g_nccl.CommInitRank(&c->comm, world, id, rank);
         if (r != ncclSuccess) { kmc_destroy(c); return fail(nullptr, KMC_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)); }
-        if (dist->fused_exchange && ndim == 2) {
+        if (dist->fused_exchange && ndim == 2) {   // (world 1: the loopback ring)
             std::string why2;
             if (!setup_fused_ipc(c, &why2)) { kmc_destroy(c); return fail(nullptr, KMC_ECUDA, "fused exchange setup: %s", why2.c_str()); }
         }
@@ -918,6 +963,8 @@ kmc_status kmc_local_shape(const kmc_ctx* c, int64_t* rl, int64_t* hl, int64_t* 
 // A validated configuration in the spare planes becomes the lattice.  Normally a pointer swap; with
 // the fused exchange the plane buffers are mapped by the neighbour ranks, so they must stay put.
 static kmc_status swap_in_spare(kmc_ctx* c) {
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     for (int p = 0; p < c->nplanes; ++p) {
         if (c->fused)
             CUDA_TRY(c, cudaMemcpyAsync(c->planes[p], c->spare[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -941,6 +988,9 @@ kmc_status kmc_set_config_device(kmc_ctx* c, const uint8_t* dev, int64_t nbytes)
     if (!c || !dev) return fail(c, KMC_EINVAL, "NULL argument");
     if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
+    CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));   // kmc_config_error reports this upload
     CUDA_TRY(c, launch_pack(c->g, dev, c->planes[0], c->nplanes > 1 ? c->planes[1] : nullptr, c->nstates, c->err_flag, c->stream));
     return KMC_OK;
 }
@@ -949,6 +999,8 @@ kmc_status kmc_get_config_device(kmc_ctx* c, uint8_t* dev, int64_t nbytes) {
     if (!c || !dev) return fail(c, KMC_EINVAL, "NULL argument");
     if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     CUDA_TRY(c, launch_unpack(c->g, c->planes[0], c->planes[1], c->nplanes, dev, c->stream));
     return KMC_OK;
 }
@@ -967,6 +1019,8 @@ kmc_status kmc_init_random(kmc_ctx* c, const double* probs, int32_t nprobs, uint
         thr[j] = cum >= 1.0 ? (1ull << 32) : (unsigned long long)std::floor(cum * 4294967296.0);
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     CUDA_TRY(c, launch_init_random(c->g, c->planes[0], c->nplanes > 1 ? c->planes[1] : nullptr, seed, thr,
                                    nprobs - 1, c->stream));
     return KMC_OK;
@@ -986,6 +1040,8 @@ kmc_status kmc_set_config(kmc_ctx* c, const uint8_t* host, int64_t nbytes) {
     for (int p = 0; p < c->nplanes; ++p)
         if (!c->spare[p] && cudaMalloc((void**)&c->spare[p], (size_t)c->plane_words * 8) != cudaSuccess)
             return fail(c, KMC_ENOMEM, "spare plane allocation failed");
+    st = fused_quiesce(c);
+    if (st != KMC_OK) return st;
     if (c->g.ghost)   // ghost rows are refreshed by the next exchange; keep them defined
         for (int p = 0; p < c->nplanes; ++p)
             CUDA_TRY(c, cudaMemcpyAsync(c->spare[p], c->planes[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -1002,6 +1058,8 @@ kmc_status kmc_get_config(kmc_ctx* c, uint8_t* host, int64_t nbytes) {
     kmc_status st = ensure_staging(c);
     if (st != KMC_OK) return st;
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     CUDA_TRY(c, launch_unpack(c->g, c->planes[0], c->planes[1], c->nplanes, c->staging, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(host, c->staging, (size_t)nbytes, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1023,6 +1081,8 @@ kmc_status kmc_set_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nword
     const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
     const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
     CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     for (int p = 0; p < c->nplanes; ++p) {
         if (c->g.ghost)   // ghost rows are refreshed by the next exchange; keep them defined
             CUDA_TRY(c, cudaMemcpyAsync(c->spare[p], c->planes[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -1077,6 +1137,8 @@ kmc_status kmc_commit_config(kmc_ctx* c) {
     if (*c->h_stage_err)
         return fail(c, KMC_EINVAL, "staged packed configuration has bits outside the cells or a site both CO and O (discarded)");
     CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->staged_ev, 0));
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     if (c->g.ghost) {   // ghost rows are refreshed by the next exchange; keep them defined (stream-ordered)
         const size_t row = (size_t)c->g.R * c->g.Mx, last = (size_t)(c->g.My_local + 1) * row;
         for (int p = 0; p < c->nplanes; ++p) {
@@ -1095,6 +1157,8 @@ kmc_status kmc_get_config_packed(kmc_ctx* c, uint64_t* host, int64_t nwords) {
     if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
     if (nwords != packed_words(c)) return fail(c, KMC_EINVAL, "nwords %lld != packed local slab %lld", (long long)nwords, packed_words(c));
     CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status sq = fused_quiesce(c);
+    if (sq != KMC_OK) return sq;
     const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
     const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
     for (int p = 0; p < c->nplanes; ++p)
@@ -1143,7 +1207,7 @@ kmc_status kmc_run_multiscale(kmc_ctx* c, double T, double dt, int32_t n_fast, k
     const uint64_t all = c->nclass >= 64 ? ~0ull : ((1ull << c->nclass) - 1ull);
     if (fast_classes == 0)   // default: the hop mechanisms (R12 diffusion, ZGB CO diffusion)
         for (int i = 0; i < c->nclass; ++i)
-            if (c->ctype[i] == T_HOP || c->ctype[i] == T_COHOP) fast_classes |= 1ull << i;
+            if (c->ctype[i] == T_HOP || c->ctype[i] == T_COHOP || c->ctype[i] == T_OHOP) fast_classes |= 1ull << i;
     fast_classes &= all;
     if (fast_classes == 0 || fast_classes == all)
         return fail(c, KMC_EINVAL, "multiscale needs a non-empty proper subset of fast classes");
@@ -1180,6 +1244,8 @@ kmc_status kmc_run_nested(kmc_ctx* c, double T, double dt, int32_t n_inner, kmc_
     kmc_status st = check_nested(c, T, dt, n_inner, outer, inner, block);
     if (st != KMC_OK) return st;
     CUDA_TRY(c, cudaSetDevice(c->device));
+    st = fused_quiesce(c);             // the exchange below reads rows the neighbours' fused windows wrote
+    if (st != KMC_OK) return st;
     bool truncated = false;
     for (double d : macro_durations(T, dt, &truncated)) {
         for (const auto& of : outer_factors(outer, d)) {
@@ -1314,8 +1380,11 @@ kmc_status kmc_vgroup_create_bounds(const kmc_geometry* geom, const kmc_model* m
         d.row_bounds = row_bounds;
         kmc_status st = create_ctx(geom, model, &d, true, &out[r]);
         if (st != KMC_OK) {
+            // ranks 0..r-1 each hold a reference: the last kmc_destroy releases the shared stream
+            // (r == 0: nobody took one, release it here); sh is not touched after that
+            const bool unowned = sh && r == 0;
             for (int q = 0; q < r; ++q) { kmc_destroy(out[q]); out[q] = nullptr; }
-            if (sh && sh->refs == 0) { cudaStreamDestroy(sh->stream); delete sh; }
+            if (unowned) { cudaStreamDestroy(sh->stream); delete sh; }
             return st;
         }
         if (sh) { out[r]->vg_shared = sh; ++sh->refs; }
@@ -1414,7 +1483,8 @@ kmc_status kmc_vgroup_run_nested(kmc_ctx** cs, int32_t world, double T, double d
 // a8 counters of the current state into out[KMC_OBS_WORDS] (device), stream-ordered: [0..35] the
 // observables kernel's counters, [36] events (all ranks), [37] windows, [38] time (double bits)
 static kmc_status enqueue_obs(kmc_ctx* c, unsigned long long* out) {
-    kmc_status st = exchange_forward(c);   // ghosts current for the +y bonds of the last owned row
+    kmc_status st = fused_quiesce(c);
+    if (st == KMC_OK) st = exchange_forward(c);   // ghosts current for the +y bonds of the last owned row
     if (st != KMC_OK) return st;
     ObsArgs a{};
     a.acc = c->obs_acc;
@@ -1467,6 +1537,10 @@ kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
         CUDA_TRY(c, cudaMemcpyAsync(wl.data(), c->wev, (size_t)owned * 4, cudaMemcpyDeviceToHost, c->stream));
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    int32_t bad = 0, timeouts = 0;
+    kmc_status se = kmc_device_errors(c, &bad, &timeouts);
+    if (se != KMC_OK) return se;
+    if (timeouts) return fail(c, KMC_ECUDA, "fused exchange: a neighbour flag wait timed out (results void)");
     decode_obs(c, c->h_obs, o);
     if (per_cell) {   // device order [cy][r][cx] -> [r][cy][cx]
         const int R = c->g.R, My = c->g.My_local, Mx = c->g.Mx;
@@ -1474,6 +1548,42 @@ kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
             for (int r = 0; r < R; ++r)
                 memcpy(per_cell + ((size_t)r * My + cy) * Mx, wl.data() + ((size_t)cy * R + r) * Mx, (size_t)Mx * 4);
     }
+    return KMC_OK;
+}
+
+kmc_status kmc_device_errors(kmc_ctx* c, int32_t* bad_spins, int32_t* wait_timeouts) {
+    if (!c) return KMC_EINVAL;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    unsigned int e = 0;
+    unsigned long long to = 0;
+    CUDA_TRY(c, cudaMemcpy(&e, c->err_flag, 4, cudaMemcpyDeviceToHost));
+    if (c->fused_ipc) CUDA_TRY(c, cudaMemcpy(&to, c->flags + 2, 8, cudaMemcpyDeviceToHost));
+    if (bad_spins) *bad_spins = e ? 1 : 0;
+    if (wait_timeouts) *wait_timeouts = to ? 1 : 0;
+    return KMC_OK;
+}
+
+kmc_status kmc_vgroup_observables(kmc_ctx** cs, int32_t world, kmc_obs* o) {
+    if (!cs || world < 2 || !o) return KMC_EINVAL;
+    kmc_ctx* c0 = cs[0];
+    for (int r = 0; r < world; ++r)
+        if (!cs[r] || !cs[r]->vgroup || cs[r]->world != world || cs[r]->rank != r)
+            return fail(c0, KMC_EINVAL, "vgroup: contexts must be ranks 0..world-1 of one kmc_vgroup_create");
+    CUDA_TRY(c0, cudaSetDevice(c0->device));
+    kmc_status st = vgroup_forward(cs, world);        // ghost rows current for the +y bonds
+    for (int r = 0; r < world && st == KMC_OK; ++r) st = enqueue_obs(cs[r], cs[r]->obs_buf);
+    if (st != KMC_OK) return st;
+    std::vector<unsigned long long> h((size_t)world * KMC_OBS_WORDS);
+    for (int r = 0; r < world; ++r)
+        CUDA_TRY(c0, cudaMemcpyAsync(h.data() + (size_t)r * KMC_OBS_WORDS, cs[r]->obs_buf, KMC_OBS_WORDS * 8,
+                                     cudaMemcpyDeviceToHost, c0->stream));
+    CUDA_TRY(c0, cudaStreamSynchronize(c0->stream));
+    // the group sum of the integer counters and event totals (words 0..36); windows and time are
+    // the same on every rank (lockstep); then the same decode as kmc_observables (R24 energy)
+    for (int r = 1; r < world; ++r)
+        for (int w = 0; w <= kObsCounters; ++w) h[(size_t)w] += h[(size_t)r * KMC_OBS_WORDS + w];
+    decode_obs(c0, h.data(), o);
     return KMC_OK;
 }
 
@@ -1492,14 +1602,15 @@ kmc_status kmc_obs_decode(const kmc_ctx* c, const uint64_t* counters, kmc_obs* o
 kmc_status kmc_correlation(kmc_ctx* c, int32_t rmax, int32_t state, int64_t* out_x, int64_t* out_y) {
     if (!c || !out_x || !out_y) return fail(c, KMC_EINVAL, "NULL argument");
     if (state < 0 || state >= c->nstates) return fail(c, KMC_EINVAL, "state %d out of range", state);
-    const long long W = c->W, H = (long long)c->g.My_local * c->g.qy * (c->world > 1 ? c->world : 1);
+    const long long W = c->W, H = c->g.ndim == 2 ? (long long)c->geom.dims[0] : 1;   // global extents
     if (rmax < 0 || rmax > kMaxCorrR || rmax >= W || (c->g.ndim == 2 && rmax >= H))
         return fail(c, KMC_EINVAL, "rmax %d out of range (< lattice extent, <= %d)", rmax, kMaxCorrR);
     const bool do_y = c->g.ndim == 2;
     if (do_y && c->g.ghost && rmax > c->g.qy)
         return fail(c, KMC_EINVAL, "multi-rank y correlation needs rmax <= q_y (one ghost cell row)");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    kmc_status st = exchange_forward(c);
+    kmc_status st = fused_quiesce(c);
+    if (st == KMC_OK) st = exchange_forward(c);
     if (st != KMC_OK) return st;
     const int R1 = rmax + 1;
     unsigned long long* d = nullptr;

@@ -19,7 +19,7 @@ constexpr int kMaxClass = 32;
 constexpr int kLogTab = 91;          // buckets of the table-driven log
 
 // Slot types, used by the host rate table.
-enum SlotType { T_ADS = 0, T_DES = 1, T_HOP = 2, T_COADS = 3, T_O2ADS = 4, T_RCO = 5, T_RO = 6, T_COHOP = 7 };
+enum SlotType { T_ADS = 0, T_DES = 1, T_HOP = 2, T_COADS = 3, T_O2ADS = 4, T_RCO = 5, T_RO = 6, T_COHOP = 7, T_OHOP = 8 };
 
 struct Geo {
     int ndim, qx, qy, nsite;
@@ -133,7 +133,7 @@ cudaError_t launch_strip_loads(const Geo& g, const uint32_t* wev, const uint32_t
                                cudaStream_t s);
 cudaError_t launch_cdf_partition(unsigned long long* loads, unsigned long long* cdf, long long M, int P, int granule,
                                  long long* out, cudaStream_t s);
-cudaError_t launch_wait_flags(const unsigned long long* flags, unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_wait_flags(unsigned long long* flags, unsigned long long epoch, cudaStream_t s);
 cudaError_t launch_signal_flags(unsigned long long* up_flags, unsigned long long* dn_flags, unsigned long long v,
                                 cudaStream_t s);
 cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* a, const uint64_t* b, long long n, cudaStream_t s);

@@ -280,6 +280,8 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         if constexpr (KIND == 4) fin = event_step_hop<NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
         else if constexpr (KIND == 5 || KIND == 6)
             fin = event_step_zgb_grouped<KIND - 3, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
+        else if constexpr (KIND == 8)
+            fin = event_step_zgb_grouped<7, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
         else fin = event_step<KIND, NDIM, MH>(a, P, h, k, tclock, gid32, have, s_logt, s_sel8);
         pend = pend || fin;
         have = have && !fin;
@@ -401,11 +403,11 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
                                 : launch_v<4, NDIM, 3, true, false>(a, nactive, s);
             }
         }
-        if constexpr (KIND == 2 || KIND == 3) {
+        if constexpr (KIND == 2 || KIND == 3 || KIND == 7) {
             // equal rates within every direction group: the grouped step (KMC_ZGBFAST=0 disables)
             static const int zf = [] { const char* e = getenv("KMC_ZGBFAST"); return e ? atoi(e) : 1; }();
             if (a.hop_fast && zf) {
-                constexpr int KG = KIND + 3;
+                constexpr int KG = KIND == 7 ? 8 : KIND + 3;
                 // launch shape measured on zgb2d_32768 (after the table-driven member boards): 256 x 3
                 // (<= 80 registers, no spill) 1.98e10 events/s; 256 x 4 (64 registers, 34-byte spill)
                 // 1.91e10; 128 x 6 1.88e10.  KMC_ZGBLB=4 selects the 4-CTA build
@@ -434,6 +436,7 @@ cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cu
     case 1: return two ? launch_t<1, 2>(a, nactive, s) : launch_t<1, 1>(a, nactive, s);
     case 2: return two ? launch_t<2, 2>(a, nactive, s) : launch_t<2, 1>(a, nactive, s);
     case 3: return two ? launch_t<3, 2>(a, nactive, s) : launch_t<3, 1>(a, nactive, s);
+    case 4: return two ? launch_t<7, 2>(a, nactive, s) : launch_t<7, 1>(a, nactive, s);   // ZGB_ODIFF
     }
     return cudaErrorInvalidValue;
 }
@@ -970,17 +973,23 @@ cudaError_t launch_cdf_partition(unsigned long long* loads, unsigned long long* 
 // (each rank's flags[0] is written by its up neighbour, flags[1] by its down neighbour, through
 // CUDA-IPC mappings over NVLink).  A rank may start window e only when both neighbours have
 // finished window e-1 (their peer writes into this rank are complete, and they no longer read the
-// rows this window will write).  One thread; a stuck neighbour traps after ~2^35 cycles instead of
-// hanging the stream.
+// rows this window will write).  One thread.  A neighbour that does not arrive within kWaitNs
+// (60 s of %globaltimer) does not hang the stream or trap the context: the kernel sets this rank's
+// timeout word flags[2] and returns; kmc_device_errors / kmc_observables report it (the run after a
+// timeout is not ordered and its results are void).
 // ---------------------------------------------------------------------------------------------
-__global__ void wait_flags_kernel(const unsigned long long* flags, unsigned long long epoch) {
-    const long long t0 = clock64();
+constexpr unsigned long long kWaitNs = 60ull * 1000000000ull;
+
+__global__ void wait_flags_kernel(unsigned long long* flags, unsigned long long epoch) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         unsigned long long a, b;
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(flags));
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(b) : "l"(flags + 1));
         if (a >= epoch && b >= epoch) return;
-        if (clock64() - t0 > (1ll << 35)) __trap();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > kWaitNs) { flags[2] = 1ull; return; }
         __nanosleep(200);
     }
 }
@@ -992,7 +1001,7 @@ __global__ void signal_flags_kernel(unsigned long long* up_flags, unsigned long 
     asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(dn_flags), "l"(v) : "memory");
 }
 
-cudaError_t launch_wait_flags(const unsigned long long* flags, unsigned long long epoch, cudaStream_t s) {
+cudaError_t launch_wait_flags(unsigned long long* flags, unsigned long long epoch, cudaStream_t s) {
     wait_flags_kernel<<<1, 1, 0, s>>>(flags, epoch);
     return cudaGetLastError();
 }

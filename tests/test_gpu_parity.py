@@ -71,6 +71,10 @@ CASES = {
     "2d_zgb": (2, (64, 64), (4, 4), "zgb", dict(k1=0.4, k2=1.0), 0, 1, None, "lie", 0.5, 3),
     "2d_zgb_diff": (2, (32, 64), (4, 8), "zgb_diff", dict(k1=0.45, k2=1.0, c_hop=1.0), 0, 2, None, "strang", 0.5, 2),
     "1d_zgb": (1, (256,), (4,), "zgb", dict(k1=0.4, k2=1.0), 0, 4, None, "random", 0.5, 3),
+    # ZGB with fast O diffusion (R33)
+    "2d_zgb_odiff": (2, (64, 32), (4, 4), "zgb_odiff", dict(k1=0.45, k2=1.0, c_hop=2.0), 0, 2, None, "lie", 0.5, 3),
+    "2d_zgb_odiff_rect": (2, (32, 64), (2, 8), "zgb_odiff", dict(k1=0.4, k2=1.0, c_hop=1.0), 0, 1, None, "strang", 0.5, 2),
+    "1d_zgb_odiff": (1, (256,), (4,), "zgb_odiff", dict(k1=0.4, k2=1.0, c_hop=3.0), 0, 4, None, "random", 0.5, 3),
 }
 
 
@@ -353,6 +357,9 @@ def test_correlation_counts_match_oracle(ndim, dims, cell, kind, R, rmax):
     (2, (64, 64), (4, 4), "adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=8.0), "lie", 4),
     (2, (32, 64), (4, 8), "zgb_diff", dict(k1=0.45, k2=1.0, c_hop=10.0), "strang", 5),
     (1, (256,), (4,), "adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-1.0, c_hop=5.0), "random", 3),
+    # the paper's named case: ZGB with fast O diffusion sub-cycled
+    (2, (64, 64), (4, 4), "zgb_odiff", dict(k1=0.45, k2=1.0, c_hop=10.0), "strang", 5),
+    (2, (32, 64), (4, 8), "zgb_odiff", dict(k1=0.4, k2=1.0, c_hop=20.0), "lie", 8),
 ])
 def test_multiscale_bit_exact(ndim, dims, cell, kind, params, inner, nf):
     """f2: kmc_run_multiscale (eq.(strang3), fast hops sub-cycled) is bit-exact vs O2."""
@@ -388,6 +395,22 @@ def test_multiscale_split_hop_blocks_bit_exact(ndim, dims, cell):
     assert orc.events > 0
 
 
+def test_multiscale_split_zgb_odiff_groups_bit_exact():
+    """ZGB_ODIFF with the O hops along x fast and along y slow (splits the hop group): the generic
+    ZGB step with the O-hop classes -- bit-exact vs O2."""
+    params = dict(k1=0.45, k2=1.0, c_hop=4.0)
+    gpu, orc = make_pair(2, (32, 32), (4, 4), "zgb_odiff", params, 0, 2)
+    lat = si.categorical_lattice(gpu.local_shape, [0.5, 0.2, 0.3], seed=15)
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    fast = [13, 14]                                  # O hops -x, +x (classes 1 + 3 z + d)
+    for _ in range(2):
+        gpu.run_multiscale(1.0, 0.5, 3, "strang", fast_classes=sum(1 << c for c in fast))
+        orc.run_multiscale(1.0, 0.5, 3, "strang", fast_classes=fast)
+        assert_same_state(gpu, orc, "multiscale split zgb_odiff groups")
+    assert orc.events > 0
+
+
 def test_multiscale_split_zgb_groups_bit_exact():
     """f2 with a fast set that splits a ZGB direction group (O2 adsorption along x fast, the rest
     slow): group rates differ within a window, so the windows run the generic ZGB step instead of
@@ -412,6 +435,7 @@ NESTED = [
     (2, (32, 64), (4, 4), "adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), 2, "lie", "random", 3),
     (1, (1024,), (32,), "adsdes", dict(ca=1, cd=1, beta=2.0, K=1.0, h=-0.5), 4, "strang", "lie", 1),
     (1, (256,), (4,), "zgb_diff", dict(k1=0.4, k2=1.0, c_hop=0.8), 8, "lie", "strang", 2),
+    (2, (64, 64), (4, 4), "zgb_odiff", dict(k1=0.45, k2=1.0, c_hop=1.5), 4, "lie", "strang", 2),
 ]
 
 
@@ -751,6 +775,7 @@ def test_workload_partition_errors():
     ("adsdes_diff", dict(ca=0.5, cd=0.5, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), (4, 4), "strang", 0.5),
     ("zgb", dict(k1=0.45, k2=1.0), (2, 4), "random", 0.5),
     ("zgb_diff", dict(k1=0.4, k2=1.0, c_hop=0.8), (4, 2), "lie", 0.25),
+    ("zgb_odiff", dict(k1=0.4, k2=1.0, c_hop=1.5), (4, 4), "strang", 0.25),
 ])
 @pytest.mark.parametrize("world", [2, 4])
 def test_fused_exchange_bit_identical(kind, params, cell, scheme, dt, world):

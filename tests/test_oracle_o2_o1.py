@@ -22,6 +22,7 @@ MODELS_1D = {
     "adsdes_diff": dict(ca=0.5, cd=1.0, beta=1.0, K=1.0, h=-1.0, c_hop=1.3),
     "zgb": dict(k1=0.4, k2=1.0),
     "zgb_diff": dict(k1=0.4, k2=1.0, c_hop=0.8),
+    "zgb_odiff": dict(k1=0.4, k2=1.0, c_hop=0.9),    # fast O diffusion (R33)
 }
 
 
@@ -228,3 +229,42 @@ def test_o2_nested_law(outer, inner, n_inner):
     check_law(confs_index(sim.get_config(), S), law)
     assert sim.window == 2 * (len(bf._inner(inner, 2, 1.0)) * n_inner * (2 if outer == "lie" else 3))
     assert int(sim.W_events.sum()) == sim.events
+
+
+def test_o2_zgb_odiff_o_hops_conserve_oxygen():
+    """P9 for the O-diffusion model (R33): windows restricted to the O-hop classes (the fast factor
+    of eq.(strang3)) move O atoms onto vacant neighbours only -- the O count per replica is
+    conserved exactly, no CO appears, and events do happen."""
+    init = np.zeros((2, 16, 16), np.uint8)
+    rng = np.random.default_rng(8)
+    init[rng.random((2, 16, 16)) < 0.4] = 2
+    p = model_params(k1=0.4, k2=1.0, c_hop=1.5)
+    sim = FSKMC(2, (16, 16), (4, 4), "zgb_odiff", p, replicas=2, seed=12)
+    sim.set_config(init)
+    hop = {i for i in range(sim.table["n"]) if int(sim.table["type"][i]) == 8}
+    assert len(hop) == 4 and all(sim.table["rate"][i] == 1.5 for i in hop)
+    for colour in range(4):
+        sim.substep(colour, 0.7, hop)
+    out = sim.get_config()
+    assert sim.events > 0
+    assert np.array_equal((out == 2).sum(axis=(1, 2)), (init == 2).sum(axis=(1, 2)))
+    assert (out == 1).sum() == 0
+
+
+@pytest.mark.parametrize("inner", ["lie", "strang"])
+def test_o2_multiscale_law_zgb_odiff(inner):
+    """f2 on the model the paper names: ZGB with fast O diffusion, the O hops as the
+    fast mechanism of eq.(strang3); O2's law = the brute-force law (8-site ring, 3^8 states)."""
+    N, q, dt, T, R, nf = 8, 2, 0.5, 1.0, 20000, 3
+    p = dict(k1=0.45, k2=1.0, c_hop=2.5)
+    lat = bf.Lattice(1, 1, N, 1, q, 2)
+    m = bf_model("zgb_odiff", p)
+    Qf, Qfc, S = bf.generators(m, lat, mech="fast")
+    Qs, Qsc, _ = bf.generators(m, lat, mech="slow")
+    assert Qf.nnz > 0 and S == 3
+    start = np.array([2, 0, 1, 2, 0, 0, 2, 0], np.uint8)
+    law = bf.law_multiscale(bf.point_mass(S, N, start), Qsc, Qfc, dt, T, nf, inner, 2)
+    sim = FSKMC(1, (N,), (q,), "zgb_odiff", model_params(**p), colours=2, replicas=R, seed=32)
+    sim.set_config(np.broadcast_to(start, (R, 1, N)))
+    sim.run_multiscale(T, dt, nf, inner)
+    check_law(confs_index(sim.get_config(), S), law)
