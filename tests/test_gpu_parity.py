@@ -484,6 +484,25 @@ def test_nested_virtual_ranks_bit_identical(kind, params, cell, block, world):
     assert a["events"] == b["events"] > 0
 
 
+def test_nested_uneven_slabs_validated_globally():
+    """f3 on uneven slabs (advisor finding): the nested geometry is checked against the GLOBAL
+    cell-row count and every slab bound, identically on every rank.  48 x 32 with 4 x 4 cells has
+    12 cell rows = 3 outer blocks of 4 (odd: blocks 0 and 2 would share an outer colour across the
+    periodic seam) -- rejected even though rank 0's slab (4 rows) x world looks fine; a bound that
+    splits an outer block is rejected too."""
+    import paper_1105_4673_b200 as kmc
+    _cuda()
+    grp = kmc.VGroup(2, (48, 32), (4, 4), kind="adsdes", row_bounds=[0, 4, 12], ca=1, cd=1, beta=1.0, K=1.0, h=-2.0)
+    with pytest.raises(kmc.KmcError) as e:
+        grp.run_nested(1.0, 0.5, 1, "lie", "lie", 4)
+    assert e.value.status == 2
+    grp = kmc.VGroup(2, (64, 32), (4, 4), kind="adsdes", row_bounds=[0, 6, 16], ca=1, cd=1, beta=1.0, K=1.0, h=-2.0)
+    with pytest.raises(kmc.KmcError) as e:
+        grp.run_nested(1.0, 0.5, 1, "lie", "lie", 4)
+    assert e.value.status == 2
+    grp.run_nested(1.0, 0.5, 1, "lie", "lie", 2)    # block 2 divides every bound: accepted
+
+
 def test_nested_errors():
     """kmc_run_nested argument checks (include/kmc.h): KMC_EINVAL / KMC_EPARTITION."""
     import paper_1105_4673_b200 as kmc
