@@ -1,11 +1,14 @@
 """Benchmark of the fractional-step KMC hot path (BASELINE.json metric: KMC events/s).
 
-python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload NAME]
+python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload NAME] [--dt DT]
 
-A step = one Lie macro-step (every colour's window: a2-a7) + the observables (a8) of the
-named workload (default: BASELINE's target, 2D Ising ads/des 32768^2, 8x8 cells, dt = 1),
-inputs resident in HBM.  N > 1: one process per GPU (torchrun), 2D slab decomposition with
-NCCL halo exchange, weak scaling (32768 x 32768 sites per GPU), max over ranks.
+A step = one macro-step of the named workload's scheme (every window of every colour: SURVEY §8(a)
+rows a2-a7) + the observables (a8), inputs resident in HBM.  Default workload: BASELINE's target
+lattice (2D Ising ads/des 32768^2, 8x8 cells) with the Strang splitting at dt = 1 -- the paper's dt
+at which the scheme also meets the north star's accuracy bar (|dtheta| <= 1e-2 vs the exact SSA,
+tests/test_gpu_statistics.py; the Lie number is `--workload ising2d_32768`).  N > 1: one process per
+GPU (this script re-launches itself under torchrun when WORLD_SIZE is unset), 2D slab decomposition
+with the NCCL halo exchange, weak scaling (one workload-sized slab per GPU), max over ranks.
 Prints ONE JSON line on rank 0.
 """
 import argparse
@@ -25,14 +28,34 @@ import synth_inputs as si  # noqa: E402
 
 METRIC = "KMC events/sec (and site-updates/sec) at 1/2/4/8 B200; % of HBM peak"
 UNIT = "events/s"
+DEFAULT_WORKLOAD = "ising2d_32768_strang"
+
+# Algorithmic work per unit ("Algorithmic work"): scalar operations the
+# method needs, independent of this implementation.
+#   one clock draw = Philox4x32-10 (10 rounds x (2 widening multiplies + 4 XOR) = 60) + U, -ln U and
+#                    tau = E / lambda with the accept test (30)                              -> 90
+#   lambda and the class walk over NC classes (count x rate, add, compare)                  -> 3 NC
+#   an executed event adds the member selection (6) and the update (4 one-site, 8 pair events)
+#   every cell-window ends with one more (rejected) clock draw (R5), which also needs lambda
+ALG_CLOCK, ALG_SELECT = 90, 6
+NCLASS_2D = {"adsdes": 7, "adsdes_diff": 22, "zgb": 13, "zgb_diff": 17, "zgb_odiff": 17}
+NCLASS_1D = {"adsdes": 5, "adsdes_diff": 9, "zgb": 7, "zgb_diff": 9, "zgb_odiff": 9}
+
+
+def alg_ops(kind, ndim, events, cell_windows):
+    nc = (NCLASS_2D if ndim == 2 else NCLASS_1D)[kind]
+    apply = 4 if kind == "adsdes" else 8
+    per_event = ALG_CLOCK + 3 * nc + ALG_SELECT + apply
+    per_window = ALG_CLOCK + 3 * nc
+    return events * per_event + cell_windows * per_window, per_event, per_window
 
 
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        return json.load(open(p)), "measured"
+        return json.load(open(p)), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -83,12 +106,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def oracle_sample(wl, sites):
+# ---------------------------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference): the O2 oracle as it stands -- the same C
+# source, single-threaded (the test build) or with the cells of a colour on all host cores (built with
+# -fopenmp, bit-identical results).  Only these legs execute oracle/.
+# ---------------------------------------------------------------------------------------------
+def cpu_model():
+    try:
+        return [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        return None
+
+
+def oracle_sample(wl, sites, seed=7):
     """A bounded sample of the workload for the O2 oracle: a side x side periodic sub-lattice in 2D,
     in 1D the workload's ring (truncated to `sites`) with as many replicas as fill `sites`."""
     from oracle.fskmc import FSKMC, model_params
     if wl["ndim"] == 2:
         side = int(round(sites ** 0.5))
+        side -= side % (2 * max(wl["cell"]))
         dims, R, desc = (side, side), 1, f"{side}x{side} periodic sub-lattice"
         shape = (1, side, side)
     else:
@@ -96,26 +132,82 @@ def oracle_sample(wl, sites):
         R = max(1, sites // N)
         dims, desc = (N,), f"{R} x {N}-site rings"
         shape = (R, 1, N)
-    o = FSKMC(wl["ndim"], dims, wl["cell"], wl["kind"], model_params(**wl["params"]), replicas=R, seed=7)
-    if wl["kind"].startswith("zgb"):
-        lat = si.categorical_lattice(shape, [1.0 - wl["init"], wl["init"] / 2, wl["init"] / 2] if wl["init"]
-                                     else [1.0, 0.0, 0.0], seed=si.SEED_BASE + 1)
-    else:
-        lat = si.bernoulli_lattice(shape, wl["init"], seed=si.SEED_BASE + 1)
-    o.set_config(lat)
+    o = FSKMC(wl["ndim"], dims, wl["cell"], wl["kind"], model_params(**wl["params"]), replicas=R, seed=seed)
+    o.set_config(initial_lattice(wl, shape, si.SEED_BASE + 1))
     return o, desc
 
 
-def cpu_baseline_sample(wl, seconds_hint="~10-30 s"):
-    """The O2 oracle as it stands, on a bounded sample of the workload (rank 0, N = 1)."""
-    o, desc = oracle_sample(wl, 512 * 512)
-    t0 = time.perf_counter()
-    nmacro = 4                                         # ~15 s of single-thread oracle work
-    o.run(nmacro * wl["dt"], wl["dt"], wl["scheme"])
+def initial_lattice(wl, shape, seed):
+    if wl["kind"].startswith("zgb"):
+        p = [1.0 - wl["init"], wl["init"] / 2, wl["init"] / 2] if wl["init"] else [1.0, 0.0, 0.0]
+        return si.categorical_lattice(shape, p, seed=seed)
+    return si.bernoulli_lattice(shape, wl["init"], seed=seed)
+
+
+def oracle_child():
+    """Child process (env BENCH_ORACLE_CHILD = JSON job): times O2 with the library ORC_LIB (the
+    OpenMP build) on a sample; prints one JSON line."""
+    job = json.loads(os.environ["BENCH_ORACLE_CHILD"])
+    wl = si.WORKLOADS[job["workload"]]
+    o, desc = oracle_sample(wl, job["sites"])
+    dt = job["dt"]
+    for _ in range(job.get("warmup", 0)):
+        o.run(dt, dt, wl["scheme"])
+    e0, t0 = o.events, time.perf_counter()
+    steps, per_step = 0, []
+    while steps < job["max_steps"]:
+        ts = time.perf_counter()
+        o.run(dt, dt, wl["scheme"])
+        o.observables()
+        per_step.append(time.perf_counter() - ts)
+        steps += 1
+        if job.get("seconds") and time.perf_counter() - t0 >= job["seconds"]:
+            break
     el = time.perf_counter() - t0
-    return {"value": o.events / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"O2 oracle, {desc} of the workload, {nmacro} {wl['scheme']} "
-                      f"macro-steps dt={wl['dt']}, {o.events} events in {el:.1f} s, 1 thread"}
+    print(json.dumps({"events": o.events - e0, "seconds": el, "steps": steps, "desc": desc,
+                      "threads": int(os.environ.get("OMP_NUM_THREADS", "1"))}), flush=True)
+
+
+def run_oracle_child(job, threads):
+    """O2 in a child process: threads > 1 -> the -fopenmp build of the same source on `threads` cores."""
+    env = dict(os.environ, BENCH_ORACLE_CHILD=json.dumps(job), OMP_NUM_THREADS=str(threads))
+    if threads > 1:
+        from oracle import _build as ob
+        env["ORC_LIB"] = ob.build_openmp(os.path.join(ROOT, "oracle", "_fskmc_oracle_omp.so"))
+    else:
+        env.pop("ORC_LIB", None)
+    r = subprocess.run([sys.executable, os.path.abspath(__file__)], env=env, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle child failed: {r.stderr[-400:]}")
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline_sample(wl_name, dt):
+    """cpu_baseline: O2 x all host cores on a bounded sample (~12 s), plus O2 x 1 and O1 x 1 (~5 s each)."""
+    wl = si.WORKLOADS[wl_name]
+    cores = os.cpu_count() or 1
+    side_cores = 1024 if wl["ndim"] == 2 else 1 << 20
+    par = run_oracle_child({"workload": wl_name, "dt": dt, "sites": side_cores ** 2 if wl["ndim"] == 2 else side_cores,
+                            "max_steps": 1000, "seconds": 12.0}, cores)
+    one = run_oracle_child({"workload": wl_name, "dt": dt, "sites": 256 * 256, "max_steps": 1000, "seconds": 5.0}, 1)
+    out = {"value": par["events"] / par["seconds"], "unit": UNIT, "cores": par["threads"], "kind": "oracle",
+           "sample": (f"O2 oracle (the plain C linear-scan oracle built with -fopenmp over the cells of a colour; "
+                      f"bit-identical to the single-thread build) on a {par['desc']} of {wl_name}, "
+                      f"{par['steps']} {wl['scheme']} macro-steps dt={dt}: {par['events']} events in "
+                      f"{par['seconds']:.1f} s on {par['threads']} threads"),
+           "cpu_model": cpu_model(), "host_cores": cores,
+           "o2_single_thread": {"value": one["events"] / one["seconds"], "unit": UNIT, "cores": 1,
+                                "sample": f"{one['desc']}, {one['steps']} macro-steps, {one['events']} events"}}
+    if wl["ndim"] == 2 and wl["kind"] == "adsdes":
+        from oracle.fskmc import model_params
+        from oracle.ssa import ssa_snapshots
+        lat = initial_lattice(wl, (1, 256, 256), si.SEED_BASE + 1)[0]
+        t0 = time.perf_counter()
+        _, nev = ssa_snapshots(lat, 2, wl["kind"], model_params(**wl["params"]), [40.0], seed=3)
+        el = time.perf_counter() - t0
+        out["o1_single_thread"] = {"value": nev / el, "unit": UNIT, "cores": 1,
+                                   "sample": f"O1 exact SSA (Fenwick tree), 256x256, T = 40: {nev} events in {el:.1f} s"}
+    return out
 
 
 L2_BYTES = 126e6                                      # B200 L2
@@ -153,31 +245,26 @@ def arm_config(workload, dt, world, fused=False, scaling="weak", loopback=False)
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (O2), timed on this host, bounded sample per step."""
+    """--impl reference: the CPU oracle O2, timed on this host's cores, a bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     wl = si.WORKLOADS[args.workload]
-    o, desc = oracle_sample(wl, 256 * 256)
     dt = args.dt if args.dt is not None else wl["dt"]
-    for _ in range(args.warmup):
-        o.run(dt, dt, wl["scheme"])
-    e0 = o.events
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        o.run(dt, dt, wl["scheme"])
-        o.observables()
-    el = time.perf_counter() - t0
-    v = (o.events - e0) / el
-    sample = f"O2 oracle on {desc} of {args.workload}, 1 macro-step per step, 1 thread"
+    cores = os.cpu_count() or 1
+    sites = 512 * 512 if wl["ndim"] == 2 else 1 << 18
+    r = run_oracle_child({"workload": args.workload, "dt": dt, "sites": sites, "max_steps": args.steps,
+                          "warmup": args.warmup}, cores)
+    v = r["events"] / r["seconds"]
+    sample = (f"O2 oracle built with -fopenmp on {r['threads']} host threads ({cpu_model()}), {r['desc']} of "
+              f"{args.workload}, one {wl['scheme']} macro-step dt={dt} + observables per step")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / max(1, args.steps),
+        "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3 / max(1, r["steps"]),
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64",
         "data": "synthetic",
-        "config": arm_config(args.workload, args.dt if args.dt is not None else wl["dt"], args.gpus,
-                             False, args.scaling),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "config": arm_config(args.workload, dt, args.gpus, False, args.scaling),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["threads"], "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -188,7 +275,7 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kmc", choices=["kmc", "reference"])
-    ap.add_argument("--workload", default="ising2d_32768", choices=sorted(si.WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(si.WORKLOADS))
     ap.add_argument("--dt", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=16)
@@ -202,12 +289,15 @@ def main():
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch this command under torchrun (the driver's own N > 1 launch
-        # sets WORLD_SIZE and lands below directly)
+        # sets WORLD_SIZE and lands below directly); NCCL's INIT lines show the communicator size
         import random
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr", "127.0.0.1", "--master-port", str(random.randint(20000, 40000)),
                os.path.abspath(__file__)] + sys.argv[1:]
-        sys.exit(subprocess.call(cmd))
+        sys.exit(subprocess.call(cmd, env=env))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -250,11 +340,7 @@ def main():
                 seed=0xB200, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=uid,
                 fused_exchange=args.fused_exchange and (world > 1 or args.loopback), **wl["params"])
     shape = k.local_shape
-    if wl["kind"].startswith("zgb"):
-        lat = si.categorical_lattice(shape, [1.0 - wl["init"], wl["init"] / 2, wl["init"] / 2] if wl["init"] else [1.0, 0.0, 0.0],
-                                     seed=si.SEED_BASE + rank)
-    else:
-        lat = si.bernoulli_lattice(shape, wl["init"], seed=si.SEED_BASE + rank)
+    lat = initial_lattice(wl, shape, si.SEED_BASE + rank)
     host = torch.from_numpy(lat).pin_memory()
     dev = host.to(f"cuda:{local}")
     # e2e input: the same lattice in the library's bit-packed upload format (1 bit per site and
@@ -263,6 +349,9 @@ def main():
     packed = si.packed_lattice(lat, ndim, wl["cell"], nplanes)
     host_pk = torch.from_numpy(packed.view(np.int64)).pin_memory()
     host_pk_np = host_pk.numpy().view(np.uint64).reshape(packed.shape)
+    # e2e result: each step's evolved packed lattice, downloaded into pinned memory
+    host_out = torch.empty(host_pk.numel(), dtype=torch.int64).pin_memory()
+    host_out_np = host_out.numpy().view(np.uint64).reshape(packed.shape)
     del lat, packed
     k.set_config_device(dev.data_ptr(), dev.numel())
     sites = int(np.prod(gdims)) * k.local_shape[0] * (world if ndim == 1 else 1)
@@ -323,40 +412,40 @@ def main():
     site_updates = sites * args.steps / (ms / 1e3)
 
     # ---- e2e: through the public API with HOST buffers, H2D + D2H inside the timed region ----
-    # the uploaded input is the lattice the timed steps reached (downloaded once, untimed), so every
-    # e2e step runs the same steady-state workload as the device-timed steps
+    # Every step uploads its packed input from pinned host memory (staged on the copy stream while
+    # the previous step runs, kmc_stage_config_packed / kmc_commit_config) and downloads its result:
+    # the observables (synchronous) and the evolved packed lattice (kmc_download_config_packed: on the
+    # copy stream, overlapping the next step, which runs on the next committed configuration).  The
+    # last download is waited for inside the timed region.  The uploaded input is the lattice the
+    # timed steps reached (downloaded once, untimed), so every e2e step runs the steady-state workload.
     host_pk_np[...] = k.get_config_packed()
     k.stage_config_packed(host_pk_np)                   # untimed e2e warm-up (first calls allocate
     k.commit_config()                                   # the spare planes and the copy stream)
     k.run(dt, dt, wl["scheme"])
+    k.download_config_packed(host_out_np)
     k.observables()
+    k.download_wait()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev_e2e = 0
     t0 = time.perf_counter()
-    e2e_parts = []
-    # every step's packed input goes host -> device inside the timed region; the copy of step s+1's
-    # input is staged (kmc_stage_config_packed, copy stream) while step s runs and committed after
-    # it (kmc_commit_config), so only the first step's upload is not overlapped
     k.stage_config_packed(host_pk_np)
     k.commit_config()
     o_prev = k.observables()
     for s_ in range(args.e2e_steps):
-        ta = time.perf_counter()
         if s_ + 1 < args.e2e_steps:
             k.stage_config_packed(host_pk_np)          # H2D of the next step's input (pinned, packed)
         k.run(dt, dt, wl["scheme"])
-        o_b = k.observables()                           # D2H of the step's result (counters)
+        k.download_config_packed(host_out_np)          # D2H of the step's evolved lattice (async)
+        o_b = k.observables()                           # D2H of the step's counters
         ev_e2e += o_b["events"] - o_prev["events"]
         o_prev = o_b
-        tb = time.perf_counter()
         if s_ + 1 < args.e2e_steps:
             k.commit_config()
-        e2e_parts.append((tb - ta, time.perf_counter() - tb))
+    k.download_wait()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    print("e2e parts (stage+run+obs s, commit s):", e2e_parts, file=sys.stderr)
     if world > 1:
         t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -367,47 +456,67 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (substep_kernel) ----
+    # ---- roofline of the dominant kernel (substep_kernel, > 98 % of a step) ----
     peaks, peak_src = load_peaks()
     avg_launch_ms = kern_ms / max(1, launches)
+    launch_s = avg_launch_ms / 1e3
     events_per_launch = events / max(1, launches) / max(1, world)      # this rank's share
-    cells_per_launch = int(np.prod(shape)) / (64 if ndim == 2 else wl["cell"][0]) / C
-    # algorithmic HBM bytes per launch: per active cell read own + 4 neighbour words
-    # and write own word (8 B each) per plane, read-modify-write 4 B of the workload counter
-    nplanes = 2 if wl["kind"].startswith("zgb") else 1
-    nb = 2 * ndim
-    bytes_per_launch = cells_per_launch * (nplanes * 8 * (nb + 2) + 8)
-    hbm_gbs = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    local_sites = int(np.prod(shape))
+    q = wl["cell"][0] * (wl["cell"][1] if ndim == 2 else 1)
+    cell_windows_per_launch = local_sites / q / C
+    # (1) issue: measured warp-instructions per event (ncu launch list of this workload at this dt,
+    #     profiles/substep_profile.json) x events per launch / launch time, against 148 SMs x 4
+    #     schedulers x f_SM -- what the kernel executes
     prof = {}
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "substep_profile.json")))
     except Exception:
         pass
-    # the per-unit figure must come from an ncu capture of this workload at this dt
-    pkey = wl["kind"] if dt == wl["dt"] else f"{wl['kind']}@dt{dt:g}"
+    pkey = args.workload if dt == si.WORKLOADS[args.workload]["dt"] else f"{args.workload}@dt{dt:g}"
     pent = prof.get(pkey, {})
-    ipe = pent.get("warp_inst_per_event") if pent.get("workload") == args.workload else None
+    ipe = pent.get("warp_inst_per_event")
     sm_clk = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     issue_peak = 148 * 4 * sm_clk * 1e6 / 1e9                              # G warp-inst / s
-    achieved = ipe * events_per_launch / (avg_launch_ms / 1e3) / 1e9 if ipe else None
+    achieved = ipe * events_per_launch / launch_s / 1e9 if ipe else None
+    # (2) algorithmic: the method's scalar operations (module constants above) / 32
+    #     lanes -- what an ideal lane-per-cell kernel would have to issue
+    ops, ops_event, ops_window = alg_ops(wl["kind"], ndim, events_per_launch, cell_windows_per_launch)
+    alg_achieved = ops / 32 / launch_s / 1e9
+    # (3) HBM: SURVEY §8(d)'s algorithmic bytes (bit-packed: read the active cells + their halo, write
+    #     the cells, + their halo for pair events; 1 bit per site and plane) beside the kernel's own
+    #     footprint (5 words read + 1 written per active cell and plane, 8 B counter RMW)
+    halo = 2 * (1 / wl["cell"][0] + 1 / wl["cell"][1]) if ndim == 2 else 2 / wl["cell"][0]
+    active_sites = local_sites / C
+    alg_bytes = nplanes * active_sites * ((1 + halo) + (1 if wl["kind"] == "adsdes" else 1 + halo)) / 8
+    foot_bytes = cell_windows_per_launch * (nplanes * 8 * (2 * ndim + 2) + 8)
+    hbm_gbs = alg_bytes / launch_s / 1e9
     roof = {"bound": "alu", "unit": "Gwarp-inst/s", "achieved": achieved, "peak": issue_peak,
             "frac": (achieved / issue_peak) if achieved else None,
             "peak_source": f"148 SMs x 4 schedulers x 1 warp-inst/clk x {sm_clk:.0f} MHz (median SM clock under load)",
-            "per_unit": f"{ipe} warp-inst/event (ncu sm__inst_executed / events, profiles/substep_profile.json)",
+            "per_unit": (f"{ipe} warp-inst/event (ncu smsp__inst_executed of this workload's launches / their events, "
+                         f"profiles/substep_profile.json[{pkey}])") if ipe else f"no ncu capture for {pkey}",
             "traffic": pent.get("dram_bytes_per_launch") if ipe else None,
-            "profile_key": pkey if ipe else None,
-            # the binding pipe (ncu capture of one window of this workload): the ALU pipe issues at
-            # half the warp-instruction rate and carries ~half the instructions of an event step
+            "frac_algorithmic": alg_achieved / issue_peak,
+            "algorithmic": {"achieved": alg_achieved, "unit": "Gwarp-inst/s",
+                            "ops_per_event": ops_event, "ops_per_cell_window": ops_window,
+                            "ops_per_launch": ops, "events_per_launch": events_per_launch,
+                            "cell_windows_per_launch": cell_windows_per_launch,
+                            "definition": "SURVEY 8(d) scalar ops (DESIGN.md 8): clock draw 90 + 3 x classes; an executed "
+                                          "event + 6 selection + 4/8 update; one rejected draw ends each cell-window; / 32 lanes"},
             "ncu_pipes": ({"alu_pipe_pct": pent.get("alu_pipe_pct"), "xu_pipe_pct": pent.get("xu_pipe_pct"),
                            "fp64_pipe_pct": pent.get("fp64_pipe_pct"), "issue_active_pct": pent.get("issue_active_pct")}
                           if ipe else None),
             "kernel": "substep_kernel", "avg_launch_ms": avg_launch_ms, "launches": launches,
             "kernel_share_of_step": kern_ms / ms,
             "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
-                    "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch}}
+                    "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": alg_bytes,
+                    "algorithmic_bytes_per_site_macro_step": alg_bytes * launches / max(1, args.steps) / local_sites,
+                    "kernel_footprint_bytes_per_launch": foot_bytes,
+                    "dram_bytes_per_launch_ncu": pent.get("dram_bytes_per_launch") if ipe else None}}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(wl)
+        cpu = cpu_baseline_sample(args.workload, dt)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -419,8 +528,11 @@ def main():
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": ev_e2e / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": int(host_pk.numel() * 8), "d2h_bytes_per_step": 2 * (37 * 8),
-                "input": "bit-packed lattice from a pinned host buffer every step (validated); the next step's upload is staged on a copy stream while the current step runs (kmc_stage_config_packed / kmc_commit_config)"},
+                "h2d_bytes_per_step": int(host_pk.numel() * 8),
+                "d2h_bytes_per_step": int(host_out.numel() * 8) + 2 * (37 * 8),
+                "steps": args.e2e_steps,
+                "input": "bit-packed lattice from a pinned host buffer every step (validated); the next step's upload is staged on a copy stream while the current step runs (kmc_stage_config_packed / kmc_commit_config)",
+                "output": "every step's evolved bit-packed lattice to pinned host memory (kmc_download_config_packed on the copy stream, overlapping the next step) + the observables counters"},
         "gpu_launches": int(launches + args.steps),
         "clocks": clocks,
     }
@@ -430,4 +542,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if os.environ.get("BENCH_ORACLE_CHILD"):
+        oracle_child()
+    else:
+        main()

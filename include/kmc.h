@@ -175,6 +175,16 @@ kmc_status kmc_set_config_packed(kmc_ctx* ctx, const uint64_t* host_words, int64
 kmc_status kmc_stage_config_packed(kmc_ctx* ctx, const uint64_t* host_words, int64_t nwords);
 kmc_status kmc_commit_config(kmc_ctx* ctx);
 kmc_status kmc_get_config_packed(kmc_ctx* ctx, uint64_t* host_words, int64_t nwords);
+/* Asynchronous download of the current packed lattice (same layout as kmc_get_config_packed): the
+ * device->host copy runs on the context's copy stream after everything enqueued so far and the call
+ * returns at once; the host buffer (pinned for a truly asynchronous copy) holds the result after
+ * kmc_download_wait (or kmc_destroy).  The device buffers being read are kept unchanged until the
+ * copy ends: a later window, exchange or upload that would overwrite them waits for it on the
+ * device, while windows that run on a configuration committed after the download
+ * (kmc_stage_config_packed / kmc_commit_config swap other buffers in) overlap it.  A second download
+ * first waits (host) for the previous one.  KMC_EINVAL on a size mismatch. */
+kmc_status kmc_download_config_packed(kmc_ctx* ctx, uint64_t* host_words, int64_t nwords);
+kmc_status kmc_download_wait(kmc_ctx* ctx);
 
 /* Advance physical time by T with macro-steps of dt (R20: n = ceil(T/dt - 1e-9) macro-steps, the
  * last of duration T - (n-1) dt; KMC_WTRUNCATED if it differs from dt).  Lie: colours 0..C-1 for

@@ -34,7 +34,8 @@ EXPORTS = [
     "kmc_vgroup_create_bounds", "kmc_workload_mark", "kmc_workload_partition", "kmc_vgroup_workload_partition",
     "kmc_vgroup_set_fused", "kmc_abi_sizes", "kmc_record_coverage", "kmc_coverage_series", "kmc_coverage_stats",
     "kmc_stage_config_packed", "kmc_commit_config", "kmc_observables_device", "kmc_obs_decode",
-    "kmc_init_random", "kmc_device_errors", "kmc_vgroup_observables",
+    "kmc_init_random", "kmc_device_errors", "kmc_vgroup_observables", "kmc_download_config_packed",
+    "kmc_download_wait",
 ]
 OBS_WORDS = 40
 KERNELS = {"auto": 0, "queue": 1, "tile": 2}
@@ -130,6 +131,8 @@ def lib():
         "kmc_coverage_stats": ([vp, i64, i32, vp, vp, i32, vp], i32),
         "kmc_device_errors": ([vp, P(i32), P(i32)], i32),
         "kmc_vgroup_observables": ([vp, i32, P(KmcObs)], i32),
+        "kmc_download_config_packed": ([vp, vp, i64], i32),
+        "kmc_download_wait": ([vp], i32),
     }
     ab_build = "KMC_B200_LIB" in os.environ          # an older build under comparison may lack new entry points
     for name, (args, res) in sig.items():
@@ -282,6 +285,20 @@ class KMC:
         out = np.empty(self.packed_shape, dtype=np.uint64)
         self._check(self._L.kmc_get_config_packed(self._ctx, out.ctypes.data, out.size))
         return out
+
+    def download_config_packed(self, out):
+        """kmc_download_config_packed: asynchronous D2H of the packed lattice into `out` (uint64
+        numpy array of packed_shape, ideally pinned); complete after download_wait()."""
+        if out.dtype != np.uint64 or out.size != int(np.prod(self.packed_shape)) or not out.flags.c_contiguous:
+            raise ValueError(f"need a C-contiguous uint64 array of {int(np.prod(self.packed_shape))} words")
+        self._check(self._L.kmc_download_config_packed(self._ctx, out.ctypes.data, out.size))
+        self._download_host = out
+
+    def download_wait(self):
+        try:
+            self._check(self._L.kmc_download_wait(self._ctx))
+        finally:
+            self._download_host = None
 
     # ---- f4: workload histogram and cdf re-partition -----------------------------
     def workload_mark(self):

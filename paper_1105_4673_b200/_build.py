@@ -31,7 +31,7 @@ def sources():
 
 
 def deps():
-    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(INCLUDE, "kmc.h"), __file__]
+    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(INCLUDE, "kmc.h"), __file__]
 
 
 def up_to_date() -> bool:

@@ -136,7 +136,10 @@ struct kmc_ctx {
     uint8_t* staging = nullptr;              // uint8 local slab (set/get_config from host)
     uint64_t* ghost_snap = nullptr;          // [2 rows][nplanes] snapshot / delta buffers (world > 1)
     uint64_t* ghost_recv = nullptr;
-    unsigned long long* h_obs = nullptr;     // pinned
+    unsigned long long* h_obs = nullptr;     // pinned, mapped: the observables kernel writes it directly
+    unsigned long long* d_hobs = nullptr;    // device alias of h_obs (no copy engine: a pending download
+                                             // on the copy stream does not delay kmc_observables)
+    unsigned long long* h_flag = nullptr;    // pinned: fused-exchange timeout word (world > 1)
     unsigned int* h_err = nullptr;           // pinned (set_config validation flag)
     uint64_t* spare[2] = {nullptr, nullptr}; // set_config double buffer
     // pipelined upload (kmc_stage_config_packed / kmc_commit_config): H2D + validation of the next
@@ -147,6 +150,11 @@ struct kmc_ctx {
     bool staged = false, consumed_valid = false;
     unsigned int* stage_err = nullptr;       // device flag of the staged check
     unsigned int* h_stage_err = nullptr;     // pinned
+    // asynchronous download (kmc_download_config_packed): D2H of the planes on the copy stream; a
+    // stream-ordered guard keeps the downloaded buffers unchanged until the copy has finished
+    cudaEvent_t dl_ev = nullptr, dl_start_ev = nullptr;
+    bool dl_pending = false;
+    const uint64_t* dl_buf = nullptr;        // planes[0] at download time (the buffer pair being read)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool vgroup = false;                     // virtual rank of a kmc_vgroup_create group (no NCCL)
@@ -282,8 +290,21 @@ kmc_status record_sample(kmc_ctx* c) {
     return KMC_OK;
 }
 
+// A pending asynchronous download reads the buffer pair whose plane 0 is dl_buf: before work on the
+// context's stream overwrites that pair (windows, exchanges, uploads), the stream waits for the copy.
+// A committed staged configuration swaps other buffers in, so the windows after it never wait.
+kmc_status dl_guard(kmc_ctx* c, const uint64_t* target) {
+    if (c->dl_pending && target == c->dl_buf) {
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->dl_ev, 0));
+        c->dl_pending = false;               // everything later on the stream is ordered after the copy
+    }
+    return KMC_OK;
+}
+
 kmc_status exchange_forward(kmc_ctx* c) {
     if (!c->comm || !c->g.ghost) return KMC_OK;   // world 1 (no ring), 1D, vgroup (exchanged by its driver)
+    kmc_status sg = dl_guard(c, c->planes[0]);
+    if (sg != KMC_OK) return sg;
     const size_t rowlen = (size_t)c->g.R * c->g.Mx;
     const int My = c->g.My_local;
     NCCL_TRY(c, g_nccl.GroupStart());
@@ -311,6 +332,8 @@ kmc_status exchange_forward(kmc_ctx* c) {
 // merged by XOR (same-colour closures are disjoint, R6, so exactly one writer per bit).
 kmc_status exchange_reverse(kmc_ctx* c) {
     if (!c->comm || !c->g.ghost || !c->cross) return KMC_OK;
+    kmc_status sg = dl_guard(c, c->planes[0]);
+    if (sg != KMC_OK) return sg;
     const size_t rowlen = (size_t)c->g.R * c->g.Mx;
     const int My = c->g.My_local;
     for (int p = 0; p < c->nplanes; ++p) {   // snap := ghost XOR snap  (the delta)
@@ -400,6 +423,8 @@ long long apply_nest(const kmc_ctx* c, const Nest& n, SubstepArgs& a) {
 }
 
 kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull, const Nest* nest = nullptr) {
+    kmc_status sg = dl_guard(c, c->planes[0]);
+    if (sg != KMC_OK) return sg;
     SubstepArgs a = c->args;
     a.plane0 = c->planes[0];                // (set_config swaps plane buffers)
     a.plane1 = c->planes[1];
@@ -888,7 +913,9 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
         ok = ok && alloc((void**)&c->ghost_snap, (size_t)4 * g.R * g.Mx * 8);
         ok = ok && alloc((void**)&c->ghost_recv, (size_t)4 * g.R * g.Mx * 8);
     }
-    ok = ok && cudaMallocHost((void**)&c->h_obs, KMC_OBS_WORDS * 8) == cudaSuccess;
+    ok = ok && cudaHostAlloc((void**)&c->h_obs, KMC_OBS_WORDS * 8, cudaHostAllocMapped) == cudaSuccess &&
+         cudaHostGetDevicePointer((void**)&c->d_hobs, c->h_obs, 0) == cudaSuccess;
+    ok = ok && cudaMallocHost((void**)&c->h_flag, 8) == cudaSuccess;
     ok = ok && cudaMallocHost((void**)&c->h_err, 4) == cudaSuccess;
     if (!ok) { kmc_destroy(c); return fail(nullptr, KMC_ENOMEM, "device allocation failed (%lld words)", c->plane_words); }
     for (int p = 0; p < c->nplanes; ++p) cudaMemsetAsync(c->planes[p], 0, (size_t)c->plane_words * 8, c->stream);
@@ -929,6 +956,8 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->copy_stream) { cudaStreamSynchronize(c->copy_stream); cudaStreamDestroy(c->copy_stream); }
     if (c->staged_ev) cudaEventDestroy(c->staged_ev);
     if (c->consumed_ev) cudaEventDestroy(c->consumed_ev);
+    if (c->dl_ev) cudaEventDestroy(c->dl_ev);
+    if (c->dl_start_ev) cudaEventDestroy(c->dl_start_ev);
     cudaFree(c->stage_err);
     if (c->h_stage_err) cudaFreeHost(c->h_stage_err);
     for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
@@ -939,6 +968,7 @@ void kmc_destroy(kmc_ctx* c) {
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv); cudaFree(c->series);
     cudaFree(c->spare[0]); cudaFree(c->spare[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);
+    if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto& pr : c->tev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -964,6 +994,7 @@ kmc_status kmc_local_shape(const kmc_ctx* c, int64_t* rl, int64_t* hl, int64_t* 
 // the fused exchange the plane buffers are mapped by the neighbour ranks, so they must stay put.
 static kmc_status swap_in_spare(kmc_ctx* c) {
     kmc_status sq = fused_quiesce(c);
+    if (sq == KMC_OK && c->fused) sq = dl_guard(c, c->planes[0]);   // fused: copied into the planes in place
     if (sq != KMC_OK) return sq;
     for (int p = 0; p < c->nplanes; ++p) {
         if (c->fused)
@@ -989,8 +1020,9 @@ kmc_status kmc_set_config_device(kmc_ctx* c, const uint8_t* dev, int64_t nbytes)
     if (nbytes != slab_bytes(c)) return fail(c, KMC_EINVAL, "nbytes %lld != local slab %lld", (long long)nbytes, slab_bytes(c));
     CUDA_TRY(c, cudaSetDevice(c->device));
     kmc_status sq = fused_quiesce(c);
+    if (sq == KMC_OK) sq = dl_guard(c, c->planes[0]);
     if (sq != KMC_OK) return sq;
-    CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));   // kmc_config_error reports this upload
+    CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));   // kmc_device_errors reports this upload
     CUDA_TRY(c, launch_pack(c->g, dev, c->planes[0], c->nplanes > 1 ? c->planes[1] : nullptr, c->nstates, c->err_flag, c->stream));
     return KMC_OK;
 }
@@ -1020,6 +1052,7 @@ kmc_status kmc_init_random(kmc_ctx* c, const double* probs, int32_t nprobs, uint
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
     kmc_status sq = fused_quiesce(c);
+    if (sq == KMC_OK) sq = dl_guard(c, c->planes[0]);
     if (sq != KMC_OK) return sq;
     CUDA_TRY(c, launch_init_random(c->g, c->planes[0], c->nplanes > 1 ? c->planes[1] : nullptr, seed, thr,
                                    nprobs - 1, c->stream));
@@ -1041,6 +1074,7 @@ kmc_status kmc_set_config(kmc_ctx* c, const uint8_t* host, int64_t nbytes) {
         if (!c->spare[p] && cudaMalloc((void**)&c->spare[p], (size_t)c->plane_words * 8) != cudaSuccess)
             return fail(c, KMC_ENOMEM, "spare plane allocation failed");
     st = fused_quiesce(c);
+    if (st == KMC_OK) st = dl_guard(c, c->spare[0]);
     if (st != KMC_OK) return st;
     if (c->g.ghost)   // ghost rows are refreshed by the next exchange; keep them defined
         for (int p = 0; p < c->nplanes; ++p)
@@ -1069,6 +1103,7 @@ kmc_status kmc_get_config(kmc_ctx* c, uint8_t* host, int64_t nbytes) {
 // Bit-packed slab: [plane][owned cell row][replica][cx] u64 words, exactly the owned rows of the
 // device planes, so H2D / D2H are one contiguous copy per plane (8x fewer bytes than uint8 sites).
 static long long packed_words(const kmc_ctx* c) { return (long long)c->nplanes * c->g.My_local * c->g.R * c->g.Mx; }
+static kmc_status ensure_copy_stream(kmc_ctx* c);
 
 kmc_status kmc_set_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nwords) {
     if (c && c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
@@ -1082,6 +1117,7 @@ kmc_status kmc_set_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nword
     const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
     CUDA_TRY(c, cudaMemsetAsync(c->err_flag, 0, 4, c->stream));
     kmc_status sq = fused_quiesce(c);
+    if (sq == KMC_OK) sq = dl_guard(c, c->spare[0]);
     if (sq != KMC_OK) return sq;
     for (int p = 0; p < c->nplanes; ++p) {
         if (c->g.ghost)   // ghost rows are refreshed by the next exchange; keep them defined
@@ -1101,13 +1137,8 @@ kmc_status kmc_stage_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nwo
     if (nwords != packed_words(c)) return fail(c, KMC_EINVAL, "nwords %lld != packed local slab %lld", (long long)nwords, packed_words(c));
     if (c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    if (!c->copy_stream) {
-        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-        CUDA_TRY(c, cudaEventCreateWithFlags(&c->staged_ev, cudaEventDisableTiming));
-        CUDA_TRY(c, cudaEventCreateWithFlags(&c->consumed_ev, cudaEventDisableTiming));
-        if (cudaMalloc((void**)&c->stage_err, 4) != cudaSuccess || cudaMallocHost((void**)&c->h_stage_err, 4) != cudaSuccess)
-            return fail(c, KMC_ENOMEM, "staging flag allocation failed");
-    }
+    kmc_status sc = ensure_copy_stream(c);
+    if (sc != KMC_OK) return sc;
     for (int p = 0; p < c->nplanes; ++p)
         if (!c->spare[p] && cudaMalloc((void**)&c->spare[p], (size_t)c->plane_words * 8) != cudaSuccess)
             return fail(c, KMC_ENOMEM, "spare plane allocation failed");
@@ -1138,6 +1169,7 @@ kmc_status kmc_commit_config(kmc_ctx* c) {
         return fail(c, KMC_EINVAL, "staged packed configuration has bits outside the cells or a site both CO and O (discarded)");
     CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->staged_ev, 0));
     kmc_status sq = fused_quiesce(c);
+    if (sq == KMC_OK && c->g.ghost) sq = dl_guard(c, c->spare[0]);   // the ghost-row copies below write the spare
     if (sq != KMC_OK) return sq;
     if (c->g.ghost) {   // ghost rows are refreshed by the next exchange; keep them defined (stream-ordered)
         const size_t row = (size_t)c->g.R * c->g.Mx, last = (size_t)(c->g.My_local + 1) * row;
@@ -1150,6 +1182,52 @@ kmc_status kmc_commit_config(kmc_ctx* c) {
     if (st != KMC_OK) return st;
     CUDA_TRY(c, cudaEventRecord(c->consumed_ev, c->stream));
     c->consumed_valid = true;
+    return KMC_OK;
+}
+
+static kmc_status ensure_copy_stream(kmc_ctx* c) {
+    if (c->copy_stream) return KMC_OK;
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->staged_ev, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->consumed_ev, cudaEventDisableTiming));
+    if (cudaMalloc((void**)&c->stage_err, 4) != cudaSuccess || cudaMallocHost((void**)&c->h_stage_err, 4) != cudaSuccess)
+        return fail(c, KMC_ENOMEM, "staging flag allocation failed");
+    return KMC_OK;
+}
+
+kmc_status kmc_download_config_packed(kmc_ctx* c, uint64_t* host, int64_t nwords) {
+    if (!c || !host) return fail(c, KMC_EINVAL, "NULL argument");
+    if (nwords != packed_words(c)) return fail(c, KMC_EINVAL, "nwords %lld != packed local slab %lld", (long long)nwords, packed_words(c));
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st = ensure_copy_stream(c);
+    if (st != KMC_OK) return st;
+    if (!c->dl_ev) {
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_ev, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_start_ev, cudaEventDisableTiming));
+    }
+    if (c->dl_pending) CUDA_TRY(c, cudaEventSynchronize(c->dl_ev));   // one download at a time
+    st = fused_quiesce(c);
+    if (st != KMC_OK) return st;
+    // the copy starts after everything enqueued on the context's stream so far
+    CUDA_TRY(c, cudaEventRecord(c->dl_start_ev, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dl_start_ev, 0));
+    const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
+    const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
+    for (int p = 0; p < c->nplanes; ++p)
+        CUDA_TRY(c, cudaMemcpyAsync(host + (size_t)p * owned, c->planes[p] + off, owned * 8, cudaMemcpyDeviceToHost,
+                                    c->copy_stream));
+    CUDA_TRY(c, cudaEventRecord(c->dl_ev, c->copy_stream));
+    c->dl_pending = true;
+    c->dl_buf = c->planes[0];
+    return KMC_OK;
+}
+
+kmc_status kmc_download_wait(kmc_ctx* c) {
+    if (!c) return KMC_EINVAL;
+    if (!c->dl_ev) return KMC_OK;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaEventSynchronize(c->dl_ev));
+    c->dl_pending = false;
     return KMC_OK;
 }
 
@@ -1527,9 +1605,13 @@ static void decode_obs(const kmc_ctx* c, const unsigned long long* h, kmc_obs* o
 kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
     if (!c || !o) return fail(c, KMC_EINVAL, "NULL argument");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    kmc_status st = enqueue_obs(c, c->obs_buf);
+    // one rank: the kernel's last block writes the counters straight into mapped pinned memory; NCCL
+    // ranks all-reduce a device buffer first, then copy
+    const bool mapped = !c->comm;
+    kmc_status st = enqueue_obs(c, mapped ? c->d_hobs : c->obs_buf);
     if (st != KMC_OK) return st;
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_obs, c->obs_buf, KMC_OBS_WORDS * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (!mapped) CUDA_TRY(c, cudaMemcpyAsync(c->h_obs, c->obs_buf, KMC_OBS_WORDS * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (c->fused_ipc) CUDA_TRY(c, cudaMemcpyAsync(c->h_flag, c->flags + 2, 8, cudaMemcpyDeviceToHost, c->stream));
     std::vector<uint32_t> wl;
     const long long owned = (long long)c->g.My_local * c->g.R * c->g.Mx;
     if (per_cell) {
@@ -1537,10 +1619,7 @@ kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
         CUDA_TRY(c, cudaMemcpyAsync(wl.data(), c->wev, (size_t)owned * 4, cudaMemcpyDeviceToHost, c->stream));
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    int32_t bad = 0, timeouts = 0;
-    kmc_status se = kmc_device_errors(c, &bad, &timeouts);
-    if (se != KMC_OK) return se;
-    if (timeouts) return fail(c, KMC_ECUDA, "fused exchange: a neighbour flag wait timed out (results void)");
+    if (c->fused_ipc && *c->h_flag) return fail(c, KMC_ECUDA, "fused exchange: a neighbour flag wait timed out (results void)");
     decode_obs(c, c->h_obs, o);
     if (per_cell) {   // device order [cy][r][cx] -> [r][cy][cx]
         const int R = c->g.R, My = c->g.My_local, Mx = c->g.Mx;

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-@pytest.mark.parametrize("workload", ["ising2d_32768", "ising1d_65536x64"])
+@pytest.mark.parametrize("workload", ["ising2d_32768_strang", "ising1d_65536x64"])
 def test_reference_arm_json_line(workload):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload",
                           workload, "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600)
@@ -24,7 +24,8 @@ def test_reference_arm_json_line(workload):
         assert key in d, key
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "events/s"
     assert d["config"]["workload"] == workload
-    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    # the oracle as it stands on all host cores (the -fopenmp build of the same C source)
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == os.cpu_count()
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
 
 
@@ -42,3 +43,15 @@ def test_config_and_l2_policy():
     # weak scaling grows the 2D lattice with the GPU count, strong scaling splits it
     assert bench.arm_config("ising2d_32768", 1.0, 8)["global_dims"] == [8 * 32768, 32768]
     assert bench.arm_config("ising2d_32768", 1.0, 8, scaling="strong")["dims_per_gpu"] == [4096, 32768]
+
+
+def test_algorithmic_op_counts():
+    """DESIGN.md §8 / SURVEY §8(d): clock draw 90 + 3 x classes; an event adds selection 6 and the
+    update (4 one-site, 8 pair); 2D Ising ads/des has 7 classes -> 121 per event, 111 per cell-window."""
+    import bench
+    ops, pe, pw = bench.alg_ops("adsdes", 2, 10, 2)
+    assert (pe, pw) == (121, 111) and ops == 10 * 121 + 2 * 111
+    _, pe, _ = bench.alg_ops("zgb", 2, 1, 0)
+    assert pe == 90 + 3 * 13 + 6 + 8
+    import synth_inputs as si
+    assert bench.DEFAULT_WORKLOAD in si.WORKLOADS and si.WORKLOADS[bench.DEFAULT_WORKLOAD]["scheme"] == "strang"

@@ -638,6 +638,50 @@ def test_staged_config_pipelined_upload(kind, dims, cell, params):
         assert np.array_equal(a.get_config(), lat1)
 
 
+@pytest.mark.parametrize("kind,dims,cell,params", [
+    ("adsdes", (64, 64), (8, 8), dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)),
+    ("zgb", (32, 32), (4, 4), dict(k1=0.4, k2=1.0)),
+])
+def test_async_download_consistent(kind, dims, cell, params):
+    """kmc_download_config_packed: the asynchronous D2H returns the lattice as of the call even when
+    windows are enqueued right after it -- in place (they wait for the copy) or on a configuration
+    committed after it (they overlap the copy) -- and the state after those windows is the same as
+    without any download."""
+    import paper_1105_4673_b200 as kmc
+    torch = _cuda()
+    a = kmc.KMC(2, dims, cell, kind=kind, replicas=2, seed=19, **params)
+    b = kmc.KMC(2, dims, cell, kind=kind, replicas=2, seed=19, **params)
+    mk = ((lambda s: si.bernoulli_lattice(a.local_shape, 0.5, seed=s)) if kind == "adsdes"
+          else (lambda s: si.categorical_lattice(a.local_shape, [0.5, 0.25, 0.25], seed=s)))
+    lat = mk(1)
+    a.set_config(lat)
+    b.set_config(lat)
+    pinned = torch.empty(int(np.prod(a.packed_shape)), dtype=torch.int64).pin_memory()
+    buf = pinned.numpy().view(np.uint64).reshape(a.packed_shape)
+    # (1) windows in place right after the download
+    a.run(1.0, 0.5, "lie")
+    a.download_config_packed(buf)
+    a.run(1.0, 0.5, "lie")
+    a.download_wait()
+    b.run(1.0, 0.5, "lie")
+    assert np.array_equal(buf, b.get_config_packed())
+    b.run(1.0, 0.5, "lie")
+    assert np.array_equal(a.get_config_packed(), b.get_config_packed())
+    # (2) stage -> run -> download -> commit -> run (the e2e pipeline of bench.py)
+    nxt = _pack_words(mk(2), cell[0], cell[1], a.packed_shape[0])
+    a.stage_config_packed(nxt)
+    a.run(1.0, 0.5, "strang")
+    a.download_config_packed(buf)
+    a.commit_config()
+    a.run(1.0, 0.5, "strang")
+    a.download_wait()
+    b.run(1.0, 0.5, "strang")
+    assert np.array_equal(buf, b.get_config_packed())
+    b.set_config_packed(nxt)
+    b.run(1.0, 0.5, "strang")
+    assert np.array_equal(a.get_config_packed(), b.get_config_packed())
+
+
 @pytest.mark.parametrize("fused", [False, True])
 def test_staged_config_on_virtual_ranks(fused):
     """The pipelined upload on the slabs of a virtual-rank group (ghost rows kept defined at the

@@ -1,10 +1,10 @@
 """Summarise an ncu capture of substep_kernel into profiles/ (run here, no GPU needed).
 
 python tools/ncu_summary.py --rep gpurun_out/prof.ncu-rep --bench gpurun_out/plain.log \
-       --kind adsdes --tag round1 [--launches gpurun_out/launches.csv]
+       --tag round2 [--launches gpurun_out/launches.csv]
 
-Writes/updates profiles/substep_profile.json ({kind: {...}}, read by bench.py for the roofline
-per-unit figure) and profiles/<tag>_substep_<kind>.md (human-readable summary).
+Writes/updates profiles/substep_profile.json ({workload[@dt]: {...}}, read by bench.py for the
+roofline per-unit figure) and profiles/<tag>_substep_<workload[@dt]>.md (human-readable summary).
 """
 import argparse
 import csv
@@ -59,12 +59,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep", required=True)
     ap.add_argument("--bench", required=True, help="bench.py JSON log of the same command")
-    ap.add_argument("--kind", default="adsdes")
+    ap.add_argument("--kind", default=None, help="profile key (default: the bench line's workload[@dt])")
     ap.add_argument("--tag", default="round1")
     ap.add_argument("--launches", default=None)
     a = ap.parse_args()
     d, stalls = read_raw(a.rep)
     b = json.loads(open(a.bench).read().strip().splitlines()[-1])
+    if a.kind is None:
+        import sys
+        sys.path.insert(0, ROOT)
+        import synth_inputs as si
+        w = b["config"]["workload"]
+        a.kind = w if b["config"]["dt"] == si.WORKLOADS[w]["dt"] else f"{w}@dt{b['config']['dt']:g}"
     C = b["config"].get("colours", 2)
     lps = {"lie": C, "strang": 2 * C - 1, "random": C}[b["config"].get("scheme", "lie")]   # windows per step
     ev_launch = b["events_per_step"] / lps

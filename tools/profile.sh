@@ -1,11 +1,11 @@
 # Profiling pass on the GPU box (one GPU): for each workload, the plain bench run first (must exit 0),
 # then the ncu launch list of the same command, then one --set full capture of one window launch.
-# Usage: bash tools/profile.sh [workload[:kind] ...]   outputs under gpurun_out/
+# Usage: bash tools/profile.sh [workload[:dt] ...]   outputs under gpurun_out/ (tag = workload[@dtDT])
 mkdir -p gpurun_out
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
-for spec in ${@:-ising2d_32768:adsdes zgb2d_32768:zgb diff2d_8192:adsdes_diff ising2d_32768:adsdes:0.01}; do
-  w=${spec%%:*}; rest=${spec#*:}; kind=${rest%%:*}; dt=${rest#*:}; [ "$dt" = "$rest" ] && dt=""
-  [ -n "$dt" ] && kind="$kind@dt$dt"
+for spec in ${@:-ising2d_32768_strang ising2d_32768 zgb2d_32768 diff2d_8192 ising2d_32768:0.01}; do
+  w=${spec%%:*}; dt=${spec#*:}; [ "$dt" = "$spec" ] && dt=""
+  kind=$w; [ -n "$dt" ] && kind="$w@dt$dt"
   CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 ${dt:+--dt $dt}"
   timeout 300 $CMD --workload $w > gpurun_out/plain_$kind.log 2> gpurun_out/plain_$kind.err; rc=$?
   echo "$w plain rc=$rc"
