@@ -296,10 +296,19 @@ kmc_status kmc_rate_table(const kmc_ctx* ctx, int32_t* n, int32_t* type, int32_t
  *   KMC_KERNEL_QUEUE: lane-per-cell kernel, per-warp cell queues, closure loaded from global memory;
  *   KMC_KERNEL_TILE:  2D spin-flip only -- a CTA stages a 32x64-cell tile + halo in shared memory and
  *                     runs its active cells from a CTA queue (best when a window holds few events);
- *   KMC_KERNEL_AUTO:  queue (measured faster in every regime on B200; env KMC_TILE=0/1 overrides).
- * Nested windows (kmc_run_nested) always use the queue kernel.
+ *   KMC_KERNEL_GROUPg (g = 2, 4, 8, 16, 32): spin flip only -- g lanes per cell: the g lanes draw g
+ *                     consecutive events' random numbers in parallel and run the serial part of the
+ *                     events in order (for windows with few active cells);
+ *   KMC_KERNEL_AUTO:  spin flip: lane groups when a window's active cells fill less than a quarter
+ *                     of the queue kernel's resident lanes (g = 2 or 4, measured best; env
+ *                     KMC_GROUP=g forces g, 1 disables), else queue; other models: queue (env
+ *                     KMC_TILE=0/1 overrides).
+ * Nested windows (kmc_run_nested) and the fused cross-GPU exchange always use the queue kernel.
  * KMC_EINVAL for an unknown mode. */
-typedef enum { KMC_KERNEL_AUTO = 0, KMC_KERNEL_QUEUE = 1, KMC_KERNEL_TILE = 2 } kmc_kernel_mode;
+typedef enum {
+    KMC_KERNEL_AUTO = 0, KMC_KERNEL_QUEUE = 1, KMC_KERNEL_TILE = 2,
+    KMC_KERNEL_GROUP2 = 3, KMC_KERNEL_GROUP4 = 4, KMC_KERNEL_GROUP8 = 5, KMC_KERNEL_GROUP16 = 6, KMC_KERNEL_GROUP32 = 7
+} kmc_kernel_mode;
 kmc_status kmc_set_kernel(kmc_ctx* ctx, int32_t mode);
 
 /* Kernel timing (bench): when enabled, every sub-step kernel is bracketed by CUDA events on the

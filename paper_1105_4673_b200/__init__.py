@@ -38,7 +38,7 @@ EXPORTS = [
     "kmc_download_wait",
 ]
 OBS_WORDS = 40
-KERNELS = {"auto": 0, "queue": 1, "tile": 2}
+KERNELS = {"auto": 0, "queue": 1, "tile": 2, "group2": 3, "group4": 4, "group8": 5, "group16": 6, "group32": 7}
 
 
 class KmcModel(ctypes.Structure):

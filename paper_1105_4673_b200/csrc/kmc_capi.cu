@@ -480,12 +480,13 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     // kernel choice: the shared-memory tile kernel for 2D spin-flip windows (KMC_TILE=0 forces the
     // lane-queue kernel, KMC_TILE=1 the tile kernel); both give bit-identical results
     static const int tile_env = [] { const char* e = getenv("KMC_TILE"); return e ? atoi(e) : -1; }();
-    int mode = c->kernel_mode;                                   // kmc_set_kernel: 0 auto, 1 queue, 2 tile
+    int mode = c->kernel_mode;                                   // kmc_set_kernel: 0 auto, 1 queue, 2 tile, 3.. groups
     if (mode == KMC_KERNEL_AUTO && tile_env >= 0) mode = tile_env ? KMC_KERNEL_TILE : KMC_KERNEL_QUEUE;
-    bool use_tile = c->kind == KMC_ADSDES && c->g.ndim == 2 && mode != KMC_KERNEL_QUEUE && !nest;
-    // auto = queue: measured on B200 the tile kernel is 4-17 % slower at dt = 1 and dt = 0.01 (both
-    // regimes are instruction-issue bound, not load-latency bound); it stays selectable
-    if (use_tile && mode == KMC_KERNEL_AUTO) use_tile = false;
+    bool use_tile = c->kind == KMC_ADSDES && c->g.ndim == 2 && mode == KMC_KERNEL_TILE && !nest;
+    // auto never picks the tile kernel: measured on B200 it is 4-17 % slower at dt = 1 and dt = 0.01
+    // (both regimes are instruction-issue bound, not load-latency bound); it stays selectable
+    // lanes per cell (spin flip): 0 = auto (group_size), 1 = the queue kernel, g = forced groups
+    a.group = mode == KMC_KERNEL_QUEUE ? 1 : mode >= KMC_KERNEL_GROUP2 ? (1 << (mode - KMC_KERNEL_GROUP2 + 1)) : 0;
     cudaError_t le = use_tile ? launch_substep_tile(a, c->stream) : cudaErrorNotSupported;
     if (le == cudaSuccess && use_tile) le = queue_slot_reset(a, c->stream);
     if (le == cudaErrorNotSupported) le = launch_substep(c->kind, a, nactive, c->stream);
@@ -1857,7 +1858,7 @@ kmc_status kmc_rate_table(const kmc_ctx* c, int32_t* n, int32_t* type, int32_t* 
 
 kmc_status kmc_set_kernel(kmc_ctx* c, int32_t mode) {
     if (!c) return KMC_EINVAL;
-    if (mode < KMC_KERNEL_AUTO || mode > KMC_KERNEL_TILE) return fail(c, KMC_EINVAL, "unknown kernel mode %d", mode);
+    if (mode < KMC_KERNEL_AUTO || mode > KMC_KERNEL_GROUP32) return fail(c, KMC_EINVAL, "unknown kernel mode %d", mode);
     c->kernel_mode = mode;
     return KMC_OK;
 }

@@ -49,6 +49,7 @@ struct SubstepArgs {
     // numbered block by block, nest_rows per block; nest_s = parity of the first local block
     // that is active.
     int refill_min;                  // parked finished lanes that trigger a warp's refill (>= 1)
+    int group;                       // lanes per cell (spin flip): 0 auto, 1 lane-per-cell kernel, g = 2..32
     int nest, nest_B, nest_s;
     uint32_t nest_rows;
     double inv_nest_rows;

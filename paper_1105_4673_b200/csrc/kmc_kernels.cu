@@ -143,47 +143,22 @@ __device__ __forceinline__ void mirror_word(const SubstepArgs& a, int p, uint32_
     else *tgt = v;
 }
 
-template <int KIND, int NDIM, int BS, int MINB, bool MH, bool NEST, bool PEER>
-__global__ void __launch_bounds__(BS, MINB)
-substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
-    using M = Model<KIND, NDIM>;
-    constexpr int NP = M::NP;
-    const Geo& g = a.g;
-    const unsigned FULL = 0xffffffffu;
-    // log_spec tables -> shared memory (lanes index them by their own bucket)
-    __shared__ double2 s_logt[kLogTab];
-    __shared__ __align__(16) uint8_t s_sel8[kSel8 + kDirTab];     // sel8 table + direction table
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
-    init_sel8(s_sel8);
-    if constexpr (KIND != 0) init_dirtab(s_sel8, g);
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // the next window's counter
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned long long cbeg64 = (unsigned long long)warp * chunk;
-    if (cbeg64 >= nactive) return;                                  // warp-uniform
-    // The grid is persistent (about one wave): warp w starts on chunk w, then claims further chunks
-    // of `chunk` cells from a global counter, so lanes never wait for a chunk boundary and there is
-    // no wave-quantisation tail -- lanes idle only in the kernel's last cell-times.
-    const unsigned long long pool0 = (unsigned long long)nwarps * chunk;   // first dynamic chunk
-    uint32_t next = (uint32_t)cbeg64 + 32;                           // warp-uniform queue head
-    uint32_t cend = (uint32_t)min(cbeg64 + chunk, (unsigned long long)nactive);
-    bool pool_open = pool0 < nactive;
-    uint64_t* planes[2] = {a.plane0, a.plane1};
-
-    uint32_t ci = (uint32_t)cbeg64 + lane;
-    bool have = ci < cend;
+// One lane's cell: the closure in registers (a3) and its write-back (a6).
+//   load: locate active cell c, its word and the four neighbour words per plane -> P, halo boards
+//   store: the cell word once per window (+ the halo deltas of hop / pair events, XOR-merged into
+//          the neighbour words: same-colour closures are disjoint, R6, so one writer per bit), the
+//          per-cell event counter (RED) and the lane's event sum
+template <int KIND, int NDIM, bool MH, bool NEST, bool PEER>
+struct Cell {
+    static constexpr int NP = Model<KIND, NDIM>::NP;
+    uint64_t P[NP], h[NP][4];
     uint32_t gid32 = 0, k = 0, iCcur = 0;
     uint32_t wrap = 0;   // hop / pair models: which neighbour indices wrap (W, E, N, S), for the store
     uint32_t srow = 0;   // PEER: storage row of the current cell
-    bool peer_wrote = false;
     double tclock = 0.0;
-    uint64_t P[NP], h[NP][4];
-    unsigned long long evsum = 0;
 
-    // a3: stage the closure (cell + one-site halo) of cell `ci` into registers
-    auto load = [&](uint32_t c) {
+    __device__ __forceinline__ void load(const SubstepArgs& a, uint64_t* const* planes, uint32_t c) {
+        const Geo& g = a.g;
         const CellLoc L = locate<NDIM, NEST>(a, c);
         gid32 = L.gid32;
         iCcur = L.iC;
@@ -198,9 +173,11 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
             P[p] = pl[L.iC];
             halo_from_words<MH>(g, pl[L.iW], pl[L.iE], NDIM == 2 ? pl[L.iN] : 0, NDIM == 2 ? pl[L.iS] : 0, h[p], NDIM == 2);
         }
-    };
-    // a6: write the cell back once per window (+ halo deltas for hop / pair events)
-    auto store = [&](uint32_t c) {
+    }
+
+    __device__ __forceinline__ void store(const SubstepArgs& a, uint64_t* const* planes, unsigned long long& evsum,
+                                          bool& peer_wrote) {
+        const Geo& g = a.g;
         if (k == 0) return;
         if constexpr (KIND == 0) {   // spin flip writes only its own word: no second locate
             planes[0][iCcur] = P[0];
@@ -216,7 +193,6 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
             return;
         }
         // neighbour indices from the cell's own index and its wrap bits (no second locate)
-        (void)c;
         const uint32_t rowlen = (uint32_t)g.R * g.Mx;
         CellLoc L;
         L.iC = iCcur;
@@ -264,7 +240,48 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
         }
         atomicAdd(&a.wev[L.iev], k);   // RED (no return): a plain += would stall on the load
         evsum += k;
-    };
+    }
+};
+
+template <int KIND, int NDIM, int BS, int MINB, bool MH, bool NEST, bool PEER>
+__global__ void __launch_bounds__(BS, MINB)
+substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk) {
+    const Geo& g = a.g;
+    const unsigned FULL = 0xffffffffu;
+    // log_spec tables -> shared memory (lanes index them by their own bucket)
+    __shared__ double2 s_logt[kLogTab];
+    __shared__ __align__(16) uint8_t s_sel8[kSel8 + kDirTab];     // sel8 table + direction table
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
+    init_sel8(s_sel8);
+    if constexpr (KIND != 0) init_dirtab(s_sel8, g);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // the next window's counter
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long cbeg64 = (unsigned long long)warp * chunk;
+    if (cbeg64 >= nactive) return;                                  // warp-uniform
+    // The grid is persistent (about one wave): warp w starts on chunk w, then claims further chunks
+    // of `chunk` cells from a global counter, so lanes never wait for a chunk boundary and there is
+    // no wave-quantisation tail -- lanes idle only in the kernel's last cell-times.
+    const unsigned long long pool0 = (unsigned long long)nwarps * chunk;   // first dynamic chunk
+    uint32_t next = (uint32_t)cbeg64 + 32;                           // warp-uniform queue head
+    uint32_t cend = (uint32_t)min(cbeg64 + chunk, (unsigned long long)nactive);
+    bool pool_open = pool0 < nactive;
+    uint64_t* planes[2] = {a.plane0, a.plane1};
+
+    uint32_t ci = (uint32_t)cbeg64 + lane;
+    bool have = ci < cend;
+    Cell<KIND, NDIM, MH, NEST, PEER> cl;
+    bool peer_wrote = false;
+    unsigned long long evsum = 0;
+    auto load = [&](uint32_t c) { cl.load(a, planes, c); };
+    auto store = [&](uint32_t) { cl.store(a, planes, evsum, peer_wrote); };
+    uint64_t* P = cl.P;
+    uint64_t (*h)[4] = cl.h;
+    uint32_t& k = cl.k;
+    double& tclock = cl.tclock;
+    const uint32_t& gid32 = cl.gid32;
 
     if (have) load(ci);
     // The event step is one branch-free basic block: lanes without a cell (queue exhausted) and
@@ -322,6 +339,87 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
     if (lane == 0 && evsum) atomicAdd(a.ev_total, evsum);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Lane-group window kernel for windows with few active cells (small lattices; SURVEY §7 step 8's
+// lanes-per-cell parameter g): G lanes own one cell.  With one lane per cell such a window has
+// too few warps to hide the latency of the serial per-event chain.  The serial part of an event
+// (neighbour boards, lambda, tau, selection, update) depends on the previous event, the draws do
+// not: the Philox block and E = -ln U of event k depend only on (k, gid, window) (R17).  So the G
+// lanes of a group draw events k .. k+G-1 in parallel (lane j: event k+j; the next batch's draws
+// are issued before this batch's serial steps, for ILP), then run the serial part of those events
+// in order -- every lane of the group on the same cell state, draw j taken from lane j by shuffle
+// -- until the cell's window ends (the first rejected draw, R5).  Same events, order and random
+// numbers as substep_kernel: bit-identical results.
+// ---------------------------------------------------------------------------------------------
+template <int KIND, int NDIM, bool MH, int G>
+__global__ void __launch_bounds__(256)
+substep_group_kernel(const SubstepArgs a, const uint32_t nactive) {
+    const Geo& g = a.g;
+    const unsigned FULL = 0xffffffffu;
+    __shared__ double2 s_logt[kLogTab];
+    __shared__ __align__(16) uint8_t s_sel8[kSel8 + kDirTab];
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
+    init_sel8(s_sel8);
+    if constexpr (KIND != 0) init_dirtab(s_sel8, g);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // as substep_kernel
+    __syncthreads();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((tid & ~31u) / G >= nactive) return;                     // warp-uniform
+    const uint32_t lane = threadIdx.x & 31u, sub = lane & (G - 1u), base = lane & ~(G - 1u);
+    const uint32_t ci = tid / G;
+    bool have = ci < nactive;
+    uint64_t* planes[2] = {a.plane0, a.plane1};
+    Cell<KIND, NDIM, MH, false, false> cl;
+    if (have) cl.load(a, planes, ci);
+    uint4 xd = philox_event(a, cl.k + sub, cl.gid32);
+    double Ed = exp_variate(a, xd, s_logt);
+    for (;;) {
+        // a cell still running after this batch has accepted all G of its events: the next batch
+        // is events k + G .. k + 2G - 1
+        const uint4 xn = philox_event(a, cl.k + G + sub, cl.gid32);
+        const double En = exp_variate(a, xn, s_logt);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int src = (int)(base | (uint32_t)j);
+            uint4 xj;
+            xj.x = 0u;
+            xj.y = 0u;
+            xj.z = __shfl_sync(FULL, xd.z, src);
+            xj.w = __shfl_sync(FULL, xd.w, src);
+            const double Ej = __hiloint2double(__shfl_sync(FULL, __double2hiint(Ed), src),
+                                               __shfl_sync(FULL, __double2loint(Ed), src));
+            bool fin;
+            if constexpr (KIND == 4)
+                fin = event_step_hop<NDIM, MH, true>(a, cl.P, cl.h, cl.k, cl.tclock, cl.gid32, have, s_logt, s_sel8, xj, Ej);
+            else if constexpr (KIND == 5 || KIND == 6)
+                fin = event_step_zgb_grouped<KIND - 3, NDIM, MH, true>(a, cl.P, cl.h, cl.k, cl.tclock, cl.gid32, have,
+                                                                       s_logt, s_sel8, xj, Ej);
+            else if constexpr (KIND == 8)
+                fin = event_step_zgb_grouped<7, NDIM, MH, true>(a, cl.P, cl.h, cl.k, cl.tclock, cl.gid32, have, s_logt,
+                                                                s_sel8, xj, Ej);
+            else
+                fin = event_step<KIND, NDIM, MH, true>(a, cl.P, cl.h, cl.k, cl.tclock, cl.gid32, have, s_logt, s_sel8, xj, Ej);
+            have = have && !fin;
+        }
+        if (!__any_sync(FULL, have)) break;
+        xd = xn;
+        Ed = En;
+    }
+    unsigned long long evsum = 0;
+    bool peer_wrote = false;
+    if (sub == 0 && ci < nactive) cl.store(a, planes, evsum, peer_wrote);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) evsum += __shfl_xor_sync(FULL, evsum, o);
+    if (lane == 0 && evsum) atomicAdd(a.ev_total, evsum);
+}
+
+template <int KIND, int NDIM, bool MH, int G>
+static cudaError_t launch_group(const SubstepArgs& a, long long nactive, cudaStream_t s) {
+    const long long threads = nactive * G;
+    substep_group_kernel<KIND, NDIM, MH, G><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a, (uint32_t)nactive);
+    return cudaGetLastError();
+}
+
 // resident CTAs per SM of one kernel instantiation (cached)
 template <typename K>
 static int resident_ctas(K kernel, int bs) {
@@ -359,6 +457,29 @@ cudaError_t queue_slot_reset(const SubstepArgs& a, cudaStream_t s) {
     return cudaMemsetAsync(a.queue + ((a.w_lo & 1u) ^ 1u), 0, sizeof(unsigned int), s);
 }
 
+// resident lanes of substep_kernel's launch shape (one lane per cell at full occupancy)
+template <int KIND, int NDIM, int MINB, bool MH>
+static long long launch_cap_lanes() {
+    static long long cap = 0;
+    if (cap == 0) cap = (long long)resident_ctas(substep_kernel<KIND, NDIM, 256, MINB, MH, false, false>, 256) * 256;
+    return cap;
+}
+
+// lanes per cell for a window of nactive cells: 1 (substep_kernel) while the cells fill a quarter
+// of the resident lanes, else the power of two (at most 4) that brings nactive x G closest to a
+// quarter of them.  Measured on B200 (tools/group_sweep.sh, events/s vs G = 1, 2, 4, 8, 16, 32):
+// 2D 1024^2 (8192 cells per window) 5.9e9 / 7.7e9 / 8.5e9 / 6.3e9 / 3.9e9 / 2.1e9; 1D 65536 (1024
+// cells) best at G = 4 (+8 %, launch-bound); 1D 1024 x 1000 replicas (16000 cells) best at G = 2
+// (+8 %); 65536 cells and more: G = 1.  Beyond G = 4 the redundant serial steps cost more issue
+// slots than the extra warps hide latency.
+static int group_size(long long nactive, long long cap_lanes) {
+    static const int env = [] { const char* e = getenv("KMC_GROUP"); return e ? atoi(e) : 0; }();
+    if (env >= 1) return env;
+    int G = 1;
+    while (G < 4 && nactive * G * 2 * 4 <= cap_lanes) G *= 2;
+    return G;
+}
+
 template <int KIND, int NDIM>
 static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_t s) {
     if (nactive <= 0) return queue_slot_reset(a, s);
@@ -369,6 +490,19 @@ static cudaError_t launch_t(const SubstepArgs& a, long long nactive, cudaStream_
     // merged halo boards need disjoint first/last columns (and rows in 2D)
     const bool mh_ok = a.g.qx >= 2 && (NDIM == 1 || a.g.qy >= 2);
     if constexpr (KIND == 0) {
+        // few active cells (small lattices): G lanes per cell (substep_group_kernel).  KMC_GROUP = G
+        // forces a group size (1 = off)
+        if (!a.nest && !a.peer_up[0]) {
+            const int G = a.group ? a.group : group_size(nactive, launch_cap_lanes<KIND, NDIM, 4, false>());
+            switch (G) {
+            case 2: return launch_group<KIND, NDIM, false, 2>(a, nactive, s);
+            case 4: return launch_group<KIND, NDIM, false, 4>(a, nactive, s);
+            case 8: return launch_group<KIND, NDIM, false, 8>(a, nactive, s);
+            case 16: return launch_group<KIND, NDIM, false, 16>(a, nactive, s);
+            case 32: return launch_group<KIND, NDIM, false, 32>(a, nactive, s);
+            default: break;
+            }
+        }
         // spin flip: the four separate (window-constant) halo boards save 8 logic ops per event and
         // measured 3 % faster at dt = 1; <= 64 registers (no spills) -> 4 CTAs of 256 per SM
         if (a.nest) return launch_v<KIND, NDIM, 4, false, true>(a, nactive, s);

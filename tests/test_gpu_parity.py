@@ -102,11 +102,17 @@ SPIN_FLIP_2D_EXTRA = {
 }
 
 
-@pytest.mark.parametrize("kernel", ["queue", "tile"])
-@pytest.mark.parametrize("name", SPIN_FLIP_2D + list(SPIN_FLIP_2D_EXTRA))
+SPIN_FLIP = [n for n, c in CASES.items() if c[3] == "adsdes"]
+
+
+@pytest.mark.parametrize("kernel", ["queue", "tile", "group2", "group8", "group32"])
+@pytest.mark.parametrize("name", SPIN_FLIP + list(SPIN_FLIP_2D_EXTRA))
 def test_bit_exact_kernel_modes(name, kernel):
-    """Both window kernels (lane-queue and shared-memory tile) are bit-exact vs O2 every window."""
+    """Every window kernel (lane-queue, shared-memory tile, g lanes per cell) is bit-exact vs O2
+    every window."""
     ndim, dims, cell, kind, params, C, R, init, scheme, dt, nmacro = {**CASES, **SPIN_FLIP_2D_EXTRA}[name]
+    if kernel == "tile" and ndim == 1:
+        pytest.skip("the tile kernel is 2D only")
     gpu, orc = make_pair(ndim, dims, cell, kind, params, C, R)
     gpu.set_kernel(kernel)
     lat = si.bernoulli_lattice(gpu.local_shape, init, seed=si.SEED_BASE + 4)
