@@ -49,7 +49,6 @@ struct SubstepArgs {
     // numbered block by block, nest_rows per block; nest_s = parity of the first local block
     // that is active.
     int refill_min;                  // parked finished lanes that trigger a warp's refill (>= 1)
-    int group;                       // lanes per cell (spin flip): 0 auto, 1 lane-per-cell kernel, g = 2..32
     int nest, nest_B, nest_s;
     uint32_t nest_rows;
     double inv_nest_rows;
@@ -70,6 +69,8 @@ struct SubstepArgs {
     uint64_t* peer_up[2];
     uint64_t* peer_dn[2];
     int peer_up_rows;                // the up neighbour's owned cell rows (its last row / bottom ghost)
+    int group;                       // lanes per cell (spin flip): 0 auto, 1 lane-per-cell kernel, g = 2..32
+                                     // (last: a field above would shift the 16-byte alignment of the round keys)
 };
 
 struct ObsArgs {

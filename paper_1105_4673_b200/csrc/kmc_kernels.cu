@@ -413,10 +413,23 @@ substep_group_kernel(const SubstepArgs a, const uint32_t nactive) {
     if (lane == 0 && evsum) atomicAdd(a.ev_total, evsum);
 }
 
+// block size: the largest of 256 / 128 / 64 threads that still gives every SM two blocks (a 1024^2
+// window is 8192 x 2 lanes: 64 blocks of 256 would leave 84 of the 148 SMs idle; 1024^2 at G = 2:
+// 7.6e9 events/s with 256-thread blocks, 9.0e9 with 64 or 128).  KMC_GROUP_BS overrides.
 template <int KIND, int NDIM, bool MH, int G>
 static cudaError_t launch_group(const SubstepArgs& a, long long nactive, cudaStream_t s) {
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
     const long long threads = nactive * G;
-    substep_group_kernel<KIND, NDIM, MH, G><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a, (uint32_t)nactive);
+    static const int bs_env = [] { const char* e = getenv("KMC_GROUP_BS"); return e ? atoi(e) : 0; }();
+    int bs = 256;
+    while (bs > 64 && (threads + bs - 1) / bs < 2LL * nsm) bs >>= 1;
+    if (bs_env == 64 || bs_env == 128 || bs_env == 256) bs = bs_env;
+    substep_group_kernel<KIND, NDIM, MH, G><<<(unsigned)((threads + bs - 1) / bs), bs, 0, s>>>(a, (uint32_t)nactive);
     return cudaGetLastError();
 }
 
@@ -465,19 +478,17 @@ static long long launch_cap_lanes() {
     return cap;
 }
 
-// lanes per cell for a window of nactive cells: 1 (substep_kernel) while the cells fill a quarter
-// of the resident lanes, else the power of two (at most 4) that brings nactive x G closest to a
-// quarter of them.  Measured on B200 (tools/group_sweep.sh, events/s vs G = 1, 2, 4, 8, 16, 32):
-// 2D 1024^2 (8192 cells per window) 5.9e9 / 7.7e9 / 8.5e9 / 6.3e9 / 3.9e9 / 2.1e9; 1D 65536 (1024
-// cells) best at G = 4 (+8 %, launch-bound); 1D 1024 x 1000 replicas (16000 cells) best at G = 2
-// (+8 %); 65536 cells and more: G = 1.  Beyond G = 4 the redundant serial steps cost more issue
-// slots than the extra warps hide latency.
+// lanes per cell for a window of nactive cells, from the queue kernel's resident lanes (148 SMs x 4
+// CTAs x 256 = 151552 on B200): G = 1 above cap/8 cells, 2 down to cap/64, else 4.  Measured on
+// B200 (tools/group_sweep.sh, KMC_GROUP = 1 / 2 / 4, events/s, with the block sizes below): 2D
+// 1024^2 (8192 cells per window) 6.0e9 / 9.0e9 / 8.4e9; 1D 65536, one replica (1024 cells,
+// launch-bound) 7.4e7 / 7.9e7 / 7.95e7; 1D 1024 x 1000 replicas (16000 cells) 1.66e9 / 1.74e9 /
+// 1.64e9; 1D 65536 x 64 replicas (65536 cells) 3.89e9 / 3.69e9 / 3.05e9.  G = 8..32 was slower
+// everywhere: the redundant serial steps cost more issue slots than the extra warps hide latency.
 static int group_size(long long nactive, long long cap_lanes) {
     static const int env = [] { const char* e = getenv("KMC_GROUP"); return e ? atoi(e) : 0; }();
     if (env >= 1) return env;
-    int G = 1;
-    while (G < 4 && nactive * G * 2 * 4 <= cap_lanes) G *= 2;
-    return G;
+    return nactive * 64 <= cap_lanes ? 4 : nactive * 8 <= cap_lanes ? 2 : 1;
 }
 
 template <int KIND, int NDIM>

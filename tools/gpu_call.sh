@@ -1,6 +1,11 @@
-# one GPU call (round 2): build, the accuracy tests, the whole -m gpu suite, the default bench line
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/c5_build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_statistics.py -q -x -k "accuracy or paper_dt" > gpurun_out/c5_stats.log 2>&1; echo "stats rc=$?"
-timeout 1500 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/c5_tests.log 2>&1; echo "tests rc=$?"
-timeout 600 python bench.py > gpurun_out/c5_bench.json 2> gpurun_out/c5_bench.err; echo "bench rc=$?"
-tail -n 3 gpurun_out/c5_stats.log gpurun_out/c5_tests.log
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "kernel_modes or every_window" > gpurun_out/g_parity.log 2>&1; echo parity rc=$?; tail -1 gpurun_out/g_parity.log
+for w in ising2d_1024 ising1d_65536 noninteracting1d_1024x1000 ising1d_65536x64; do
+  for G in 1 2 4; do
+    for BS in 64 128 256; do
+      [ $G = 1 ] && [ $BS != 64 ] && continue
+      export KMC_GROUP=$G KMC_GROUP_BS=$BS
+      timeout 120 python bench.py --no-cpu-baseline --workload $w --steps 50 --warmup 5 --e2e-steps 0 2>/dev/null | tail -1 | python -c "import json,sys;d=json.load(sys.stdin);print('$w G=$G bs=$BS', '%.4g'%d['value'], 'ms/step %.4g'%d['ms_per_step'], 'share %.3f'%d['roofline']['kernel_share_of_step'])"
+    done
+  done
+done
