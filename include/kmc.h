@@ -233,7 +233,10 @@ kmc_status kmc_observables(kmc_ctx* ctx, kmc_obs* out, uint32_t* per_cell_events
  * ordered nearest-neighbour bonds (x, x+e), e in {+x, +y}, [a*4 + b], [36] events, [37] windows,
  * [38] time (IEEE double bits), [39] 0.  Stream-ordered, asynchronous; world > 1 sums words 0..36
  * over the NCCL ranks (collective).  kmc_obs_decode turns a host copy of those words into a kmc_obs
- * (what kmc_observables returns for the same state). */
+ * (what kmc_observables returns for the same state).  The vacant-state entries are completed from
+ * the lattice identities (every site has one +e neighbour and is the +e neighbour of one site), so a
+ * single virtual rank's words (kmc_vgroup_create) are contributions whose sum mod 2^64 over the
+ * group is the count, not counts of that slab. */
 #define KMC_OBS_WORDS 40
 kmc_status kmc_observables_device(kmc_ctx* ctx, uint64_t* dev_counters);
 /* Device-side error words (synchronises the context's stream): *bad_spins = 1 if the last

@@ -136,20 +136,38 @@ def test_library_schedule_matches_oracle_run(scheme):
     assert abs(gpu.get_state()[1] - 2.5) < 1e-12
 
 
-def test_observables_match_oracle():
-    for kind, params, init in [("adsdes", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), 0.5),
-                               ("zgb", dict(k1=0.4, k2=1.0), None)]:
-        gpu, orc = make_pair(2, (64, 96), (4, 8), kind, params, 0, 2)
-        lat = (si.bernoulli_lattice(gpu.local_shape, 0.4, seed=3) if init is not None
-               else si.categorical_lattice(gpu.local_shape, [0.5, 0.3, 0.2], seed=3))
-        gpu.set_config(lat); orc.set_config(lat)
-        gpu.run(1.0, 0.5, "lie"); orc.run(1.0, 0.5, "lie")
-        a, b = gpu.observables(), orc.observables()
-        for key in ("n_state", "nn_pairs", "n_state_by_colour"):
-            assert np.array_equal(a[key], b[key]), (kind, key, a[key], b[key])
-        assert a["events"] == b["events"] and a["windows"] == b["windows"]
-        assert np.allclose(a["coverage"], b["coverage"], rtol=0, atol=1e-15)
-        assert abs(a["energy"] - b["energy"]) <= 1e-9 * max(1.0, abs(b["energy"]))
+@pytest.mark.parametrize("kind,ndim,dims,cell,colours,replicas", [
+    ("adsdes", 2, (64, 96), (4, 8), 0, 2),
+    ("zgb", 2, (64, 96), (4, 8), 0, 2),             # 3 states, 4 colours
+    ("adsdes", 2, (48, 80), (2, 2), 4, 3),          # spin flip with 4 colours
+    ("adsdes", 1, (512,), (8,), 0, 5),              # 1D rings (one +e bond per site)
+    ("zgb_odiff", 1, (256,), (4,), 0, 3),
+    ("adsdes", 2, (16, 16), (1, 1), 0, 1),          # 1-site cells
+    ("adsdes_diff", 2, (24, 40), (4, 4), 0, 7),     # ragged: rows of 10 cells, 7 replicas
+    # rows of 128 cells: the kernel's row-aligned fast path (one locate per 128 cells, +x words by shuffle)
+    ("adsdes", 1, (1024,), (8,), 0, 3),
+    ("zgb", 2, (16, 1024), (4, 8), 0, 2),
+    ("adsdes", 2, (32, 2048), (8, 8), 0, 1),        # 256 cells per row, 4 cell rows
+])
+def test_observables_match_oracle(kind, ndim, dims, cell, colours, replicas):
+    """a8 counters (sites per state, by colour, unordered bonds), coverage and energy = the oracle's
+    (itself pinned by hand-counted lattices, tests/test_oracle_observables.py).  The kernel counts
+    only the occupied states and completes the vacant entries from the lattice identities."""
+    params = {"adsdes": dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), "zgb": dict(k1=0.4, k2=1.0),
+              "zgb_odiff": dict(k1=0.4, k2=1.0, c_hop=1.0),
+              "adsdes_diff": dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0, c_hop=1.0)}[kind]
+    init = None if kind.startswith("zgb") else 0.5
+    gpu, orc = make_pair(ndim, dims, cell, kind, params, colours, replicas)
+    lat = (si.bernoulli_lattice(gpu.local_shape, 0.4, seed=3) if init is not None
+           else si.categorical_lattice(gpu.local_shape, [0.5, 0.3, 0.2], seed=3))
+    gpu.set_config(lat); orc.set_config(lat)
+    gpu.run(1.0, 0.5, "lie"); orc.run(1.0, 0.5, "lie")
+    a, b = gpu.observables(), orc.observables()
+    for key in ("n_state", "nn_pairs", "n_state_by_colour"):
+        assert np.array_equal(a[key], b[key]), (kind, key, a[key], b[key])
+    assert a["events"] == b["events"] and a["windows"] == b["windows"]
+    assert np.allclose(a["coverage"], b["coverage"], rtol=0, atol=1e-15)
+    assert abs(a["energy"] - b["energy"]) <= 1e-9 * max(1.0, abs(b["energy"]))
 
 
 @pytest.mark.parametrize("kind,ndim,dims,cell", [("adsdes", 2, (64, 64), (8, 8)), ("zgb", 2, (32, 32), (4, 4)),
