@@ -422,15 +422,16 @@ long long apply_nest(const kmc_ctx* c, const Nest& n, SubstepArgs& a) {
     return half * c->g.R * (long long)n_o * a.nest_rows;
 }
 
-kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull, const Nest* nest = nullptr) {
-    kmc_status sg = dl_guard(c, c->planes[0]);
-    if (sg != KMC_OK) return sg;
+// The kernel arguments of window c->window + ahead (colour, duration D; class_mask: multiscale rate
+// subset; nest: f3 outer blocks) and its number of active cells.
+static SubstepArgs window_args(const kmc_ctx* c, int colour, double D, uint64_t class_mask, const Nest* nest,
+                               uint64_t ahead, long long* nactive_out) {
     SubstepArgs a = c->args;
     a.plane0 = c->planes[0];                // (set_config swaps plane buffers)
     a.plane1 = c->planes[1];
     a.colour = colour;
     a.D = D;
-    const long long nactive = nest ? apply_nest(c, *nest, a) : active_cells(c);
+    *nactive_out = nest ? apply_nest(c, *nest, a) : active_cells(c);
     if (c->fused && !nest) {
         for (int p = 0; p < 2; ++p) { a.peer_up[p] = c->peer_up[p]; a.peer_dn[p] = c->peer_dn[p]; }
         a.peer_up_rows = c->peer_up_rows;
@@ -444,8 +445,9 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
     static const int refill_hi[5] = {3, 4, 6, 6, 6}, refill_lo[5] = {10, 10, 16, 16, 16};   // by model kind
     a.refill_min = refill_env >= 1 && refill_env <= 32 ? refill_env
                  : (D * c->rate_per_cell >= 16.0 ? refill_hi[c->kind] : refill_lo[c->kind]);
-    a.w_lo = (uint32_t)c->window;
-    a.w_hi_tag = (uint32_t)((c->window >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
+    const uint64_t w = c->window + ahead;
+    a.w_lo = (uint32_t)w;
+    a.w_hi_tag = (uint32_t)((w >> 32) & 0x0FFFFFFFu);   // tag EVT = 0 (R17)
     if (class_mask != ~0ull)
         for (int i = 0; i < c->nclass; ++i) a.rate[i] = ((class_mask >> i) & 1ull) ? c->crate_u64[i] : 0ull;
     if (c->kind == KMC_ADSDES_DIFF) {   // R31 hop blocks: one rate per block -> the block-walk kernel
@@ -464,34 +466,49 @@ kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask =
         for (int i = 1; i < c->nclass; ++i)
             a.hop_fast &= a.rate[i] == a.rate[1 + ((i - 1) / z) * z] ? 1 : 0;
     }
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (c->timing) {
-        if (c->tev_used == c->tev.size()) {
-            cudaEvent_t x, y;
-            CUDA_TRY(c, cudaEventCreate(&x));
-            CUDA_TRY(c, cudaEventCreate(&y));
-            c->tev.emplace_back(x, y);
-        }
-        e0 = c->tev[c->tev_used].first;
-        e1 = c->tev[c->tev_used].second;
-        ++c->tev_used;
-        CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+    // lanes per cell (spin flip): 0 = auto (group_size), 1 = the queue kernel, g = forced groups
+    const int mode = c->kernel_mode;
+    a.group = mode == KMC_KERNEL_QUEUE ? 1 : mode >= KMC_KERNEL_GROUP2 ? (1 << (mode - KMC_KERNEL_GROUP2 + 1)) : 0;
+    return a;
+}
+
+// kernel timing (kmc_enable_timing): an event pair around a launch
+static kmc_status timing_begin(kmc_ctx* c, cudaEvent_t* e1) {
+    *e1 = nullptr;
+    if (!c->timing) return KMC_OK;
+    if (c->tev_used == c->tev.size()) {
+        cudaEvent_t x, y;
+        CUDA_TRY(c, cudaEventCreate(&x));
+        CUDA_TRY(c, cudaEventCreate(&y));
+        c->tev.emplace_back(x, y);
     }
+    *e1 = c->tev[c->tev_used].second;
+    CUDA_TRY(c, cudaEventRecord(c->tev[c->tev_used].first, c->stream));
+    ++c->tev_used;
+    return KMC_OK;
+}
+
+kmc_status launch_window(kmc_ctx* c, int colour, double D, uint64_t class_mask = ~0ull, const Nest* nest = nullptr) {
+    kmc_status sg = dl_guard(c, c->planes[0]);
+    if (sg != KMC_OK) return sg;
+    long long nactive = 0;
+    SubstepArgs a = window_args(c, colour, D, class_mask, nest, 0, &nactive);
+    cudaEvent_t e1 = nullptr;
+    kmc_status st = timing_begin(c, &e1);
+    if (st != KMC_OK) return st;
     // kernel choice: the shared-memory tile kernel for 2D spin-flip windows (KMC_TILE=0 forces the
     // lane-queue kernel, KMC_TILE=1 the tile kernel); both give bit-identical results
     static const int tile_env = [] { const char* e = getenv("KMC_TILE"); return e ? atoi(e) : -1; }();
     int mode = c->kernel_mode;                                   // kmc_set_kernel: 0 auto, 1 queue, 2 tile, 3.. groups
     if (mode == KMC_KERNEL_AUTO && tile_env >= 0) mode = tile_env ? KMC_KERNEL_TILE : KMC_KERNEL_QUEUE;
-    bool use_tile = c->kind == KMC_ADSDES && c->g.ndim == 2 && mode == KMC_KERNEL_TILE && !nest;
     // auto never picks the tile kernel: measured on B200 it is 4-17 % slower at dt = 1 and dt = 0.01
     // (both regimes are instruction-issue bound, not load-latency bound); it stays selectable
-    // lanes per cell (spin flip): 0 = auto (group_size), 1 = the queue kernel, g = forced groups
-    a.group = mode == KMC_KERNEL_QUEUE ? 1 : mode >= KMC_KERNEL_GROUP2 ? (1 << (mode - KMC_KERNEL_GROUP2 + 1)) : 0;
+    const bool use_tile = c->kind == KMC_ADSDES && c->g.ndim == 2 && mode == KMC_KERNEL_TILE && !nest;
     cudaError_t le = use_tile ? launch_substep_tile(a, c->stream) : cudaErrorNotSupported;
     if (le == cudaSuccess && use_tile) le = queue_slot_reset(a, c->stream);
     if (le == cudaErrorNotSupported) le = launch_substep(c->kind, a, nactive, c->stream);
     CUDA_TRY(c, le);
-    if (c->timing) CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+    if (e1) CUDA_TRY(c, cudaEventRecord(e1, c->stream));
     c->window += 1;
     return KMC_OK;
 }

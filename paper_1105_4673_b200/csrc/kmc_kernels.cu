@@ -351,20 +351,12 @@ substep_kernel(const SubstepArgs a, const uint32_t nactive, const uint32_t chunk
 // -- until the cell's window ends (the first rejected draw, R5).  Same events, order and random
 // numbers as substep_kernel: bit-identical results.
 // ---------------------------------------------------------------------------------------------
+// One window of the lane-group scheme for this thread's group (cell tid / G); returns the lane's
+// event count (nonzero only in sub-lane 0, which writes the cell back).
 template <int KIND, int NDIM, bool MH, int G>
-__global__ void __launch_bounds__(256)
-substep_group_kernel(const SubstepArgs a, const uint32_t nactive) {
-    const Geo& g = a.g;
+__device__ __forceinline__ unsigned long long group_window(const SubstepArgs& a, uint32_t nactive, uint32_t tid,
+                                                           const double2* s_logt, const uint8_t* s_sel8) {
     const unsigned FULL = 0xffffffffu;
-    __shared__ double2 s_logt[kLogTab];
-    __shared__ __align__(16) uint8_t s_sel8[kSel8 + kDirTab];
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
-    init_sel8(s_sel8);
-    if constexpr (KIND != 0) init_dirtab(s_sel8, g);
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // as substep_kernel
-    __syncthreads();
-    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
-    if ((tid & ~31u) / G >= nactive) return;                     // warp-uniform
     const uint32_t lane = threadIdx.x & 31u, sub = lane & (G - 1u), base = lane & ~(G - 1u);
     const uint32_t ci = tid / G;
     bool have = ci < nactive;
@@ -408,9 +400,33 @@ substep_group_kernel(const SubstepArgs a, const uint32_t nactive) {
     unsigned long long evsum = 0;
     bool peer_wrote = false;
     if (sub == 0 && ci < nactive) cl.store(a, planes, evsum, peer_wrote);
+    return evsum;
+}
+
+template <int KIND>
+__device__ __forceinline__ void group_tables(const SubstepArgs& a, double2* s_logt, uint8_t* s_sel8) {
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_logt[i] = a.logtab[i];
+    init_sel8(s_sel8);
+    if constexpr (KIND != 0) init_dirtab(s_sel8, a.g);
+}
+
+__device__ __forceinline__ void add_events(unsigned long long evsum, unsigned long long* total) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) evsum += __shfl_xor_sync(FULL, evsum, o);
-    if (lane == 0 && evsum) atomicAdd(a.ev_total, evsum);
+    for (int o = 16; o > 0; o >>= 1) evsum += __shfl_xor_sync(0xffffffffu, evsum, o);
+    if ((threadIdx.x & 31u) == 0 && evsum) atomicAdd(total, evsum);
+}
+
+template <int KIND, int NDIM, bool MH, int G>
+__global__ void __launch_bounds__(256)
+substep_group_kernel(const SubstepArgs a, const uint32_t nactive) {
+    __shared__ double2 s_logt[kLogTab];
+    __shared__ __align__(16) uint8_t s_sel8[kSel8 + kDirTab];
+    group_tables<KIND>(a, s_logt, s_sel8);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.queue[(a.w_lo & 1u) ^ 1u] = 0u;   // as substep_kernel
+    __syncthreads();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((tid & ~31u) / G >= nactive) return;                     // warp-uniform
+    add_events(group_window<KIND, NDIM, MH, G>(a, nactive, tid, s_logt, s_sel8), a.ev_total);
 }
 
 // block size: the largest of 256 / 128 / 64 threads that still gives every SM two blocks (a 1024^2

@@ -136,6 +136,31 @@ def test_library_schedule_matches_oracle_run(scheme):
     assert abs(gpu.get_state()[1] - 2.5) < 1e-12
 
 
+@pytest.mark.parametrize("kernel", ["auto", "group2", "group4"])
+@pytest.mark.parametrize("ndim,dims,cell,colours,scheme,dt", [
+    (2, (64, 64), (8, 8), 0, "lie", 1.0),
+    (2, (64, 64), (8, 8), 0, "strang", 0.7),
+    (2, (48, 80), (2, 2), 4, "strang", 0.5),         # 7 windows per macro-step
+    (2, (32, 64), (4, 4), 4, "random", 0.5),
+    (1, (1024,), (32,), 0, "random", 1.0),
+    (1, (512,), (8,), 0, "strang", 0.5),
+])
+def test_group_kernel_run_matches_oracle_run(kernel, ndim, dims, cell, colours, scheme, dt):
+    """kmc_run's own schedule on small spin-flip lattices (the lane-group kernel, auto or forced g)
+    with 2 and 4 colours: the lattice, the per-cell event counts and the totals equal the oracle's
+    run() after every call, including a truncated last step (R20)."""
+    p = dict(ca=1, cd=1, beta=1.3, K=1.0, h=-2.0 if ndim == 2 else -1.0)
+    gpu, orc = make_pair(ndim, dims, cell, "adsdes", p, colours, 3)
+    gpu.set_kernel(kernel)
+    lat = si.bernoulli_lattice(gpu.local_shape, 0.5, seed=11)
+    gpu.set_config(lat)
+    orc.set_config(lat)
+    for T in (2 * dt, 2.5 * dt):
+        assert gpu.run(T, dt, scheme) == orc.run(T, dt, scheme)
+        assert_same_state(gpu, orc, f"{scheme} T={T}")
+    assert orc.events > 0
+
+
 @pytest.mark.parametrize("kind,ndim,dims,cell,colours,replicas", [
     ("adsdes", 2, (64, 96), (4, 8), 0, 2),
     ("zgb", 2, (64, 96), (4, 8), 0, 2),             # 3 states, 4 colours
