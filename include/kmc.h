@@ -149,10 +149,27 @@ kmc_status kmc_get_config(kmc_ctx* ctx, uint8_t* host_local_slab, int64_t nbytes
  * whether the last kmc_set_config_device had any.  The lattice stays in the library's bit-packed
  * device planes (8x smaller than the uint8 buffer): the caller's buffer is read (set)
  * or written (get) during the call's stream work only and is never borrowed -- the uint8 site-major
- * layout of §8(b)'s borrowed kmc_dist.lattice cannot be the working layout of the bit-board kernels,
- * so kmc_dist has no such field; kmc_set/get_config_packed move the working layout itself. */
+ * layout of §8(b)'s borrowed kmc_dist.lattice cannot be the working layout of the bit-board kernels;
+ * the borrowed buffer is the bit-packed working planes instead (kmc_attach_planes below). */
 kmc_status kmc_set_config_device(kmc_ctx* ctx, const uint8_t* dev_local_slab, int64_t nbytes);
 kmc_status kmc_get_config_device(kmc_ctx* ctx, uint8_t* dev_local_slab, int64_t nbytes);
+/* Borrowed working lattice (§8(b)'s borrowed device buffer, in the kernels' own layout): after
+ * kmc_attach_planes the windows, exchanges and observables run on the caller's device buffer
+ * `dev_planes` (e.g. a torch int64 CUDA tensor's data_ptr, 8-byte aligned, on the context's device)
+ * of nwords = planes x words_per_plane u64: plane p at dev_planes + p x words_per_plane, each plane
+ * [storage row][replica][cell column] with storage rows = the owned cell rows plus, when the
+ * context has ghost rows (2D, world > 1 or the loopback ring), one ghost row above and below
+ * (owned row i at storage row i + ghost); a word's bit (ly*q_x + lx) is the site (cy*q_y + ly,
+ * cx*q_x + lx) -- the kmc_set_config_packed layout plus the ghost rows.  The call copies the
+ * current lattice in (stream-ordered) and frees the library's own planes; from then on the buffer
+ * always holds the current lattice (configuration uploads copy into it instead of swapping
+ * buffers) and it is never freed by the library: the caller keeps it alive until kmc_destroy.
+ * kmc_planes_layout reports the sizes (before or after attaching).  KMC_EINVAL on a size mismatch
+ * or a misaligned / NULL pointer; KMC_ESTATE with the fused exchange (its CUDA-IPC mappings are
+ * made at create) or while a staged upload is pending. */
+kmc_status kmc_planes_layout(const kmc_ctx* ctx, int32_t* planes, int64_t* words_per_plane, int64_t* storage_rows,
+                             int32_t* ghost);
+kmc_status kmc_attach_planes(kmc_ctx* ctx, uint64_t* dev_planes, int64_t nwords);
 /* Bit-packed local slab (host buffers; the checkpoint format and the cheap upload path -- 1 bit per
  * site and plane instead of 1 byte per site): nwords = planes x rows_local/q_y x replicas_local x
  * W/q_x u64 words in the library's own layout [plane][cell row][replica][cell column] (DESIGN.md

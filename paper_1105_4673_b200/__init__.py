@@ -26,6 +26,7 @@ NSTATES = {0: 2, 1: 2, 2: 3, 3: 3, 4: 3}
 EXPORTS = [
     "kmc_create", "kmc_destroy", "kmc_last_error", "kmc_create_error", "kmc_local_shape",
     "kmc_set_config", "kmc_get_config", "kmc_set_config_device", "kmc_get_config_device",
+    "kmc_planes_layout", "kmc_attach_planes",
     "kmc_run", "kmc_substep", "kmc_observables", "kmc_get_state", "kmc_set_state",
     "kmc_rate_table", "kmc_enable_timing", "kmc_timing", "kmc_partition_plan",
     "kmc_nccl_unique_id", "kmc_version", "kmc_vgroup_create", "kmc_vgroup_run", "kmc_vgroup_sync",
@@ -93,6 +94,8 @@ def lib():
         "kmc_set_config": ([vp, vp, i64], i32),
         "kmc_get_config": ([vp, vp, i64], i32),
         "kmc_set_config_device": ([vp, vp, i64], i32),
+        "kmc_planes_layout": ([vp, vp, vp, vp, vp], i32),
+        "kmc_attach_planes": ([vp, vp, i64], i32),
         "kmc_get_config_device": ([vp, vp, i64], i32),
         "kmc_run": ([vp, dbl, dbl, i32], i32),
         "kmc_substep": ([vp, i32, dbl], i32),
@@ -316,6 +319,18 @@ class KMC:
 
     def get_config_device(self, ptr, nbytes):
         self._check(self._L.kmc_get_config_device(self._ctx, ctypes.c_void_p(ptr), int(nbytes)))
+
+    def planes_layout(self):
+        """kmc_planes_layout: {'planes', 'words_per_plane', 'storage_rows', 'ghost'} of the working lattice."""
+        n, w, r, gh = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        self._check(self._L.kmc_planes_layout(self._ctx, ctypes.byref(n), ctypes.byref(w), ctypes.byref(r),
+                                              ctypes.byref(gh)))
+        return {"planes": n.value, "words_per_plane": w.value, "storage_rows": r.value, "ghost": gh.value}
+
+    def attach_planes(self, ptr, nwords):
+        """kmc_attach_planes: run on the caller's device buffer (e.g. a torch int64 CUDA tensor's
+        data_ptr(), kept alive by the caller until close) as the working lattice."""
+        self._check(self._L.kmc_attach_planes(self._ctx, ctypes.c_void_p(ptr), int(nwords)))
 
     # ---- the hot path --------------------------------------------------------
     def run(self, T, dt, scheme="lie"):

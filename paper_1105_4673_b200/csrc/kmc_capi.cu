@@ -112,6 +112,7 @@ struct kmc_ctx {
     uint32_t* wev = nullptr;
     uint32_t* wmark = nullptr;               // f4: per-cell counters at the last kmc_workload_mark
     bool fused = false;                      // fused halo exchange (peer writes inside the window kernel)
+    bool borrowed = false;                   // planes are the caller's buffer (kmc_attach_planes)
     bool fused_ipc = false;                  // ... across GPUs: CUDA-IPC peer planes + device flags
     unsigned long long* flags = nullptr;     // [2]: written by the up / down neighbour
     unsigned long long* peer_up_flags = nullptr;
@@ -980,7 +981,8 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->h_stage_err) cudaFreeHost(c->h_stage_err);
     for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
-    for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
+    if (!c->borrowed)
+        for (int p = 0; p < 2; ++p) cudaFree(c->planes[p]);
     cudaFree(c->flags);
     cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->obs_acc); cudaFree(c->logtab); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv); cudaFree(c->series);
@@ -1012,14 +1014,50 @@ kmc_status kmc_local_shape(const kmc_ctx* c, int64_t* rl, int64_t* hl, int64_t* 
 // the fused exchange the plane buffers are mapped by the neighbour ranks, so they must stay put.
 static kmc_status swap_in_spare(kmc_ctx* c) {
     kmc_status sq = fused_quiesce(c);
-    if (sq == KMC_OK && c->fused) sq = dl_guard(c, c->planes[0]);   // fused: copied into the planes in place
+    const bool in_place = c->fused || c->borrowed;   // mapped by the neighbours / the caller's buffer
+    if (sq == KMC_OK && in_place) sq = dl_guard(c, c->planes[0]);   // copied into the planes in place
     if (sq != KMC_OK) return sq;
     for (int p = 0; p < c->nplanes; ++p) {
-        if (c->fused)
+        if (in_place)
             CUDA_TRY(c, cudaMemcpyAsync(c->planes[p], c->spare[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
         else
             std::swap(c->spare[p], c->planes[p]);
     }
+    return KMC_OK;
+}
+
+kmc_status kmc_planes_layout(const kmc_ctx* c, int32_t* planes, int64_t* words_per_plane, int64_t* storage_rows,
+                             int32_t* ghost) {
+    if (!c) return KMC_EINVAL;
+    if (planes) *planes = c->nplanes;
+    if (words_per_plane) *words_per_plane = c->plane_words;
+    if (storage_rows) *storage_rows = c->g.My_local + 2 * c->g.ghost;
+    if (ghost) *ghost = c->g.ghost;
+    return KMC_OK;
+}
+
+kmc_status kmc_attach_planes(kmc_ctx* c, uint64_t* dev, int64_t nwords) {
+    if (!c || !dev) return fail(c, KMC_EINVAL, "NULL argument");
+    if (((uintptr_t)dev & 7u) != 0) return fail(c, KMC_EINVAL, "dev_planes must be 8-byte aligned");
+    if (nwords != (int64_t)c->nplanes * c->plane_words)
+        return fail(c, KMC_EINVAL, "nwords %lld != %d planes x %lld words", (long long)nwords, c->nplanes, c->plane_words);
+    if (c->fused) return fail(c, KMC_ESTATE, "borrowed planes with the fused exchange (IPC mappings made at create)");
+    if (c->staged) return fail(c, KMC_ESTATE, "a staged configuration is pending (kmc_commit_config first)");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    kmc_status st = dl_guard(c, c->planes[0]);
+    if (st != KMC_OK) return st;
+    if (c->dl_pending) CUDA_TRY(c, cudaEventSynchronize(c->dl_ev));   // a download reads the old planes
+    c->dl_pending = false;
+    uint64_t* old[2] = {c->planes[0], c->planes[1]};
+    for (int p = 0; p < c->nplanes; ++p)
+        CUDA_TRY(c, cudaMemcpyAsync(dev + (size_t)p * c->plane_words, old[p], (size_t)c->plane_words * 8,
+                                    cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int p = 0; p < c->nplanes; ++p) {
+        if (!c->borrowed) cudaFree(old[p]);
+        c->planes[p] = dev + (size_t)p * c->plane_words;
+    }
+    c->borrowed = true;
     return KMC_OK;
 }
 

@@ -677,6 +677,8 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
             const int col = a.C == 2 ? (NDIM == 1 ? (int)(cx & 1) : (int)((cx + gy) & 1)) : (int)(cx & 1) + 2 * (int)(gy & 1);
             // the word after the block: the next cell of the row, or its first cell (periodic wrap)
             const uint32_t iNext = cx0 + 32u * U == (uint32_t)g.Mx ? iC0 + 32u * U - (uint32_t)g.Mx : iC0 + 32u * U;
+            KMC_BOUNDS(cx0 + 32u * U <= (uint32_t)g.Mx && iS0 + 32u * U <= (uint32_t)(g.My_local + 2 * g.ghost) * rowlen &&
+                       iC0 + 32u * U <= (uint32_t)(g.My_local + 2 * g.ghost) * rowlen);
             uint64_t Pw[U][NP], Sw[U][NP], Nx[NP];
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
@@ -721,6 +723,8 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
                 iC[u] = (uint32_t)sy * rowlen + r * g.Mx + cx;
                 cxv[u] = cx;
                 const uint32_t iS = (uint32_t)syS * rowlen + r * g.Mx + cx;
+                KMC_BOUNDS(!ok[u] || (iC[u] < (uint32_t)(g.My_local + 2 * g.ghost) * rowlen &&
+                                      iS < (uint32_t)(g.My_local + 2 * g.ghost) * rowlen));
                 const uint32_t gy = g.row_offset + cy;
                 col[u] = a.C == 2 ? (NDIM == 1 ? (int)(cx & 1) : (int)((cx + gy) & 1)) : (int)(cx & 1) + 2 * (int)(gy & 1);
 #pragma unroll

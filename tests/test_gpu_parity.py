@@ -955,3 +955,58 @@ def test_maximum_size_lattice():
     assert outs[0] == outs[1]
     with pytest.raises(kmc.KmcError):
         kmc.KMC(2, (n, n), (8, 8), kind="adsdes", replicas=65, seed=5, **p)   # 65 x 2^26 cells > 2^32
+
+
+@pytest.mark.parametrize("kind,ndim,dims,cell,loopback", [
+    ("adsdes", 2, (64, 64), (8, 8), False),
+    ("zgb", 2, (32, 64), (4, 8), False),
+    ("adsdes_diff", 2, (64, 32), (4, 4), True),       # ghost rows: the NCCL loopback ring
+    ("adsdes", 1, (1024,), (32,), False),
+])
+def test_borrowed_planes(kind, ndim, dims, cell, loopback):
+    """kmc_attach_planes (§8(b) borrowed device buffer): the windows run on a caller-owned torch
+    tensor that always holds the current packed lattice (owned rows = get_config_packed, ghost rows
+    around them); configuration uploads copy into it; results are bit-identical to a context on its
+    own planes; the tensor outlives the context."""
+    torch = _cuda()
+    import paper_1105_4673_b200 as kmc
+    params = {"adsdes": dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0), "zgb": dict(k1=0.4, k2=1.0),
+              "adsdes_diff": dict(ca=1, cd=1, beta=1.0, K=1.0, h=-2.0, c_hop=1.0)}[kind]
+    extra = dict(nccl_id=kmc.nccl_unique_id()) if loopback else {}
+    a = kmc.KMC(ndim, dims, cell, kind=kind, replicas=2, seed=21, **params)
+    b = kmc.KMC(ndim, dims, cell, kind=kind, replicas=2, seed=21, **params, **extra)
+    init = (lambda s: si.categorical_lattice(a.local_shape, [0.5, 0.25, 0.25], seed=s)) if kind == "zgb" else \
+           (lambda s: si.bernoulli_lattice(a.local_shape, 0.5, seed=s))
+    lat = init(3)
+    a.set_config(lat)
+    b.set_config(lat)
+    lay = b.planes_layout()
+    assert lay["ghost"] == (1 if loopback else 0)
+    buf = torch.full((lay["planes"] * lay["words_per_plane"],), -1, dtype=torch.int64, device="cuda")
+    with pytest.raises(kmc.KmcError):
+        b.attach_planes(buf.data_ptr(), buf.numel() - 1)
+    b.attach_planes(buf.data_ptr(), buf.numel())
+
+    def owned_rows():
+        torch.cuda.synchronize()
+        v = buf.cpu().numpy().view(np.uint64).reshape(lay["planes"], lay["storage_rows"], -1)
+        gh = lay["ghost"]
+        return v[:, gh:lay["storage_rows"] - gh].reshape(b.packed_shape)
+
+    assert np.array_equal(owned_rows(), b.get_config_packed())
+    for i in range(3):
+        a.run(1.0, 0.5, "strang")
+        b.run(1.0, 0.5, "strang")
+        assert np.array_equal(a.get_config(), b.get_config()), i
+        assert np.array_equal(owned_rows(), b.get_config_packed()), i
+        assert a.observables()["events"] == b.observables()["events"]
+    lat2 = init(4)                                      # an upload lands in the borrowed buffer
+    a.set_config(lat2)
+    b.set_config(lat2)
+    assert np.array_equal(owned_rows(), a.get_config_packed())
+    a.run(1.0, 0.5, "lie")
+    b.run(1.0, 0.5, "lie")
+    assert np.array_equal(a.get_config(), b.get_config())
+    last = b.get_config_packed()
+    b.close()
+    assert np.array_equal(owned_rows(), last)           # the caller's tensor outlives the context
