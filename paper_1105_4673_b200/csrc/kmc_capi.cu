@@ -143,9 +143,12 @@ struct kmc_ctx {
     unsigned long long* h_flag = nullptr;    // pinned: fused-exchange timeout word (world > 1)
     unsigned int* h_err = nullptr;           // pinned (set_config validation flag)
     uint64_t* spare[2] = {nullptr, nullptr}; // set_config double buffer
+    uint64_t* spare2[2] = {nullptr, nullptr};// third buffer: a staged upload while the previous planes download
     // pipelined upload (kmc_stage_config_packed / kmc_commit_config): H2D + validation of the next
     // configuration into the spare planes on a copy stream, overlapping the windows in flight
-    cudaStream_t copy_stream = nullptr;
+    cudaStream_t copy_stream = nullptr;      // H2D of staged uploads
+    cudaStream_t dl_stream = nullptr;        // D2H of kmc_download_config_packed (own stream: the PCIe
+                                             // link is full duplex, so a download overlaps the next upload)
     cudaEvent_t staged_ev = nullptr;         // copy + check of the staged configuration done
     cudaEvent_t consumed_ev = nullptr;       // every window that read the current spare has been enqueued before it
     bool staged = false, consumed_valid = false;
@@ -973,6 +976,7 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->fused_ipc && c->flags && c->stream) launch_wait_flags(c->flags, c->epoch, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) { cudaStreamSynchronize(c->copy_stream); cudaStreamDestroy(c->copy_stream); }
+    if (c->dl_stream) { cudaStreamSynchronize(c->dl_stream); cudaStreamDestroy(c->dl_stream); }
     if (c->staged_ev) cudaEventDestroy(c->staged_ev);
     if (c->consumed_ev) cudaEventDestroy(c->consumed_ev);
     if (c->dl_ev) cudaEventDestroy(c->dl_ev);
@@ -986,7 +990,7 @@ void kmc_destroy(kmc_ctx* c) {
     cudaFree(c->flags);
     cudaFree(c->wev); cudaFree(c->wmark); cudaFree(c->strips); cudaFree(c->wl_out); cudaFree(c->ev_total); cudaFree(c->queue); cudaFree(c->obs_buf); cudaFree(c->obs_acc); cudaFree(c->logtab); cudaFree(c->err_flag);
     cudaFree(c->staging); cudaFree(c->ghost_snap); cudaFree(c->ghost_recv); cudaFree(c->series);
-    cudaFree(c->spare[0]); cudaFree(c->spare[1]);
+    cudaFree(c->spare[0]); cudaFree(c->spare[1]); cudaFree(c->spare2[0]); cudaFree(c->spare2[1]);
     if (c->h_obs) cudaFreeHost(c->h_obs);
     if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->h_err) cudaFreeHost(c->h_err);
@@ -1201,8 +1205,17 @@ kmc_status kmc_stage_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nwo
     const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
     const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
     cudaStream_t cs = c->copy_stream;
-    // the spare planes were the current planes before the last commit: the windows enqueued before
-    // it may still read them
+    // a pending download (its own stream) may still read the spare planes -- the planes current
+    // before the last commit: stage into a third buffer instead, so that the upload overlaps the
+    // download (buffers rotate current -> downloading -> staging)
+    if (c->dl_pending && c->dl_buf == c->spare[0]) {
+        for (int p = 0; p < c->nplanes; ++p)
+            if (!c->spare2[p] && cudaMalloc((void**)&c->spare2[p], (size_t)c->plane_words * 8) != cudaSuccess)
+                return fail(c, KMC_ENOMEM, "third plane buffer allocation failed");
+        for (int p = 0; p < c->nplanes; ++p) std::swap(c->spare[p], c->spare2[p]);
+    }
+    // the spare planes were current before an earlier commit: the windows enqueued before the last
+    // commit may still read them
     if (c->consumed_valid) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->consumed_ev, 0));
     CUDA_TRY(c, cudaMemsetAsync(c->stage_err, 0, 4, cs));
     for (int p = 0; p < c->nplanes; ++p)
@@ -1258,6 +1271,7 @@ kmc_status kmc_download_config_packed(kmc_ctx* c, uint64_t* host, int64_t nwords
     kmc_status st = ensure_copy_stream(c);
     if (st != KMC_OK) return st;
     if (!c->dl_ev) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->dl_stream, cudaStreamNonBlocking));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_ev, cudaEventDisableTiming));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_start_ev, cudaEventDisableTiming));
     }
@@ -1266,13 +1280,13 @@ kmc_status kmc_download_config_packed(kmc_ctx* c, uint64_t* host, int64_t nwords
     if (st != KMC_OK) return st;
     // the copy starts after everything enqueued on the context's stream so far
     CUDA_TRY(c, cudaEventRecord(c->dl_start_ev, c->stream));
-    CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dl_start_ev, 0));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->dl_stream, c->dl_start_ev, 0));
     const size_t owned = (size_t)c->g.My_local * c->g.R * c->g.Mx;
     const size_t off = (size_t)c->g.ghost * c->g.R * c->g.Mx;
     for (int p = 0; p < c->nplanes; ++p)
         CUDA_TRY(c, cudaMemcpyAsync(host + (size_t)p * owned, c->planes[p] + off, owned * 8, cudaMemcpyDeviceToHost,
-                                    c->copy_stream));
-    CUDA_TRY(c, cudaEventRecord(c->dl_ev, c->copy_stream));
+                                    c->dl_stream));
+    CUDA_TRY(c, cudaEventRecord(c->dl_ev, c->dl_stream));
     c->dl_pending = true;
     c->dl_buf = c->planes[0];
     return KMC_OK;

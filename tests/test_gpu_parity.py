@@ -731,6 +731,35 @@ def test_async_download_consistent(kind, dims, cell, params):
     assert np.array_equal(a.get_config_packed(), b.get_config_packed())
 
 
+def test_e2e_pipeline_every_download():
+    """bench.py's end-to-end loop for several steps on an 8192^2 lattice with short windows (so that
+    each step's download is still in flight when the next step's upload is staged): every step's
+    downloaded lattice equals a synchronous reference -- the staged upload goes to a third plane
+    buffer, never into the planes being downloaded."""
+    import paper_1105_4673_b200 as kmc
+    torch = _cuda()
+    p = dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0)
+    a = kmc.KMC(2, (8192, 8192), (8, 8), kind="adsdes", seed=23, **p)
+    b = kmc.KMC(2, (8192, 8192), (8, 8), kind="adsdes", seed=23, **p)
+    ins = [_pack_words(si.bernoulli_lattice(a.local_shape, 0.2 + 0.1 * i, seed=40 + i), 8, 8, 1) for i in range(4)]
+    outs = [torch.empty(int(np.prod(a.packed_shape)), dtype=torch.int64).pin_memory() for _ in range(6)]
+    bufs = [o.numpy().view(np.uint64).reshape(a.packed_shape) for o in outs]
+    a.stage_config_packed(ins[0])
+    a.commit_config()
+    for s in range(6):
+        if s + 1 < 6:
+            a.stage_config_packed(ins[(s + 1) % 4])
+        a.run(0.02, 0.01, "lie")
+        a.download_config_packed(bufs[s])
+        if s + 1 < 6:
+            a.commit_config()
+    a.download_wait()
+    for s in range(6):
+        b.set_config_packed(ins[s % 4])
+        b.run(0.02, 0.01, "lie")
+        assert np.array_equal(bufs[s], b.get_config_packed()), s
+
+
 @pytest.mark.parametrize("fused", [False, True])
 def test_staged_config_on_virtual_ranks(fused):
     """The pipelined upload on the slabs of a virtual-rank group (ghost rows kept defined at the
