@@ -75,6 +75,10 @@ CASES = {
     "2d_zgb_odiff": (2, (64, 32), (4, 4), "zgb_odiff", dict(k1=0.45, k2=1.0, c_hop=2.0), 0, 2, None, "lie", 0.5, 3),
     "2d_zgb_odiff_rect": (2, (32, 64), (2, 8), "zgb_odiff", dict(k1=0.4, k2=1.0, c_hop=1.0), 0, 1, None, "strang", 0.5, 2),
     "1d_zgb_odiff": (1, (256,), (4,), "zgb_odiff", dict(k1=0.4, k2=1.0, c_hop=3.0), 0, 4, None, "random", 0.5, 3),
+    # 8 x 8 cells: the window kernels built with the cell shape as a compile-time constant
+    "2d_zgb_8x8": (2, (64, 128), (8, 8), "zgb", dict(k1=0.42, k2=1.0), 0, 1, None, "lie", 0.5, 3),
+    "2d_zgb_diff_8x8": (2, (64, 64), (8, 8), "zgb_diff", dict(k1=0.4, k2=1.0, c_hop=1.0), 0, 2, None, "strang", 0.5, 2),
+    "2d_zgb_odiff_8x8": (2, (64, 64), (8, 8), "zgb_odiff", dict(k1=0.4, k2=1.0, c_hop=2.0), 0, 1, None, "random", 0.5, 3),
 }
 
 
