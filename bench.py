@@ -278,7 +278,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(si.WORKLOADS))
     ap.add_argument("--dt", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="steps of the end-to-end measurement (default: --steps, like the device-timed loop)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: one workload-sized slab per GPU (default); strong: the workload split over the GPUs")
     ap.add_argument("--fused-exchange", action="store_true",
@@ -287,6 +288,8 @@ def main():
                     help="N = 1, 2D: run the lattice as a one-rank ring through the multi-GPU data plane "
                          "(NCCL send/recv to itself, or the fused exchange) to measure its cost on one GPU")
     args = ap.parse_args()
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch this command under torchrun (the driver's own N > 1 launch
         # sets WORLD_SIZE and lands below directly); NCCL's INIT lines show the communicator size
