@@ -633,7 +633,7 @@ cudaError_t launch_substep(int kind, const SubstepArgs& a, long long nactive, cu
 // cells' loads in flight (the grid-stride loop is otherwise latency-bound: round 1 measured
 // ~1.3 TB/s on the 128 MiB target lattice).
 // ---------------------------------------------------------------------------------------------
-template <int NP, int NDIM>
+template <int NP, int NDIM, int SQ = 0>
 __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
     constexpr int U = 4;
     const unsigned FULL = 0xffffffffu;
@@ -659,12 +659,13 @@ __global__ void __launch_bounds__(256) observables_kernel(const ObsArgs a) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint64_t* planes[2] = {a.plane0, a.plane1};
     // counts of one cell from its planes P, the +x neighbour words E and the +y neighbour words S
+    const int qx = SQ > 0 ? SQ : g.qx, shN = SQ > 0 ? SQ * (SQ - 1) : g.shN;   // SQ: compile-time 8 x 8 cells
     auto count = [&](const uint64_t* P, const uint64_t* E, const uint64_t* S, int col) {
         uint64_t Bx[NP], By[NP];
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            Bx[p] = ((P[p] >> 1) & g.notcolL) | ((E[p] << (g.qx - 1)) & g.colL);                // sigma(x + e_x)
-            By[p] = NDIM == 2 ? ((P[p] >> g.qx) | ((S[p] << g.shN) & g.rowL)) : 0ull;            // sigma(x + e_y)
+            Bx[p] = ((P[p] >> 1) & g.notcolL) | ((E[p] << (qx - 1)) & g.colL);                  // sigma(x + e_x)
+            By[p] = NDIM == 2 ? ((P[p] >> qx) | ((S[p] << shN) & g.rowL)) : 0ull;                // sigma(x + e_y)
         }
 #pragma unroll
         for (int s = 0; s < NP; ++s) {
@@ -1069,11 +1070,14 @@ cudaError_t launch_observables(const ObsArgs& a, cudaStream_t s) {
     long long nb = (ncell + 255) / 256;
     if (nb > 4LL * nsm) nb = 4LL * nsm;
     if (nb < 1) nb = 1;
+    const bool q8 = a.g.ndim == 2 && a.g.qx == 8 && a.g.qy == 8;
     if (a.nplanes == 1) {
-        if (a.g.ndim == 2) observables_kernel<1, 2><<<(unsigned)nb, 256, 0, s>>>(a);
+        if (q8) observables_kernel<1, 2, 8><<<(unsigned)nb, 256, 0, s>>>(a);
+        else if (a.g.ndim == 2) observables_kernel<1, 2><<<(unsigned)nb, 256, 0, s>>>(a);
         else observables_kernel<1, 1><<<(unsigned)nb, 256, 0, s>>>(a);
     } else {
-        if (a.g.ndim == 2) observables_kernel<2, 2><<<(unsigned)nb, 256, 0, s>>>(a);
+        if (q8) observables_kernel<2, 2, 8><<<(unsigned)nb, 256, 0, s>>>(a);
+        else if (a.g.ndim == 2) observables_kernel<2, 2><<<(unsigned)nb, 256, 0, s>>>(a);
         else observables_kernel<2, 1><<<(unsigned)nb, 256, 0, s>>>(a);
     }
     return cudaGetLastError();
