@@ -417,10 +417,12 @@ def main():
     # ---- e2e: through the public API with HOST buffers, H2D + D2H inside the timed region ----
     # Every step uploads its packed input from pinned host memory (staged on the copy stream while
     # the previous step runs, kmc_stage_config_packed / kmc_commit_config) and downloads its result:
-    # the observables (synchronous) and the evolved packed lattice (kmc_download_config_packed: on the
-    # copy stream, overlapping the next step, which runs on the next committed configuration).  The
-    # last download is waited for inside the timed region.  The uploaded input is the lattice the
-    # timed steps reached (downloaded once, untimed), so every e2e step runs the steady-state workload.
+    # the observables counters (kmc_observables_device + an asynchronous copy into pinned host memory,
+    # decoded by kmc_obs_decode after the loop: no host synchronisation per step) and the evolved
+    # packed lattice (kmc_download_config_packed: on its own stream, overlapping the next step, which
+    # runs on the next committed configuration).  Every copy is complete inside the timed region.
+    # The uploaded input is the lattice the timed steps reached (downloaded once, untimed), so every
+    # e2e step runs the steady-state workload.
     host_pk_np[...] = k.get_config_packed()
     k.stage_config_packed(host_pk_np)                   # untimed e2e warm-up (first calls allocate
     k.commit_config()                                   # the spare planes and the copy stream)
@@ -431,24 +433,28 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev_e2e = 0
+    ne = max(1, args.e2e_steps)
+    cnt_dev = torch.zeros((ne + 1, kmc.OBS_WORDS), dtype=torch.int64, device=f"cuda:{local}")
+    cnt_host = torch.zeros((ne + 1, kmc.OBS_WORDS), dtype=torch.int64).pin_memory()
     t0 = time.perf_counter()
     k.stage_config_packed(host_pk_np)
     k.commit_config()
-    o_prev = k.observables()
+    k.observables_device(cnt_dev[0].data_ptr())
+    cnt_host[0].copy_(cnt_dev[0], non_blocking=True)
     for s_ in range(args.e2e_steps):
         if s_ + 1 < args.e2e_steps:
             k.stage_config_packed(host_pk_np)          # H2D of the next step's input (pinned, packed)
         k.run(dt, dt, wl["scheme"])
         k.download_config_packed(host_out_np)          # D2H of the step's evolved lattice (async)
-        o_b = k.observables()                           # D2H of the step's counters
-        ev_e2e += o_b["events"] - o_prev["events"]
-        o_prev = o_b
+        k.observables_device(cnt_dev[s_ + 1].data_ptr())
+        cnt_host[s_ + 1].copy_(cnt_dev[s_ + 1], non_blocking=True)   # D2H of the step's counters (async)
         if s_ + 1 < args.e2e_steps:
             k.commit_config()
     k.download_wait()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    cnt_np = cnt_host.numpy()
+    ev_e2e = k.obs_decode(cnt_np[args.e2e_steps])["events"] - k.obs_decode(cnt_np[0])["events"]
     if world > 1:
         t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -532,10 +538,10 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": ev_e2e / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(host_pk.numel() * 8),
-                "d2h_bytes_per_step": int(host_out.numel() * 8) + 2 * (37 * 8),
+                "d2h_bytes_per_step": int(host_out.numel() * 8) + int(cnt_host.shape[1]) * 8,
                 "steps": args.e2e_steps,
                 "input": "bit-packed lattice from a pinned host buffer every step (validated); the next step's upload is staged on a copy stream while the current step runs (kmc_stage_config_packed / kmc_commit_config)",
-                "output": "every step's evolved bit-packed lattice to pinned host memory (kmc_download_config_packed on the copy stream, overlapping the next step) + the observables counters"},
+                "output": "every step's evolved bit-packed lattice to pinned host memory (kmc_download_config_packed on its own stream, overlapping the next step) + the step's observables counters (kmc_observables_device, copied asynchronously to pinned memory, decoded with kmc_obs_decode)"},
         "gpu_launches": int(launches + args.steps),
         "clocks": clocks,
     }
