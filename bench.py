@@ -436,18 +436,27 @@ def main():
     ne = max(1, args.e2e_steps)
     cnt_dev = torch.zeros((ne + 1, kmc.OBS_WORDS), dtype=torch.int64, device=f"cuda:{local}")
     cnt_host = torch.zeros((ne + 1, kmc.OBS_WORDS), dtype=torch.int64).pin_memory()
+
+    def counters(i):
+        # one rank: the observables kernel writes the pinned host words directly (no copy-engine
+        # transfer that would queue behind the lattice download); NCCL ranks all-reduce a device
+        # buffer, then copy it
+        if world == 1:
+            k.observables_device(cnt_host[i].data_ptr())
+        else:
+            k.observables_device(cnt_dev[i].data_ptr())
+            cnt_host[i].copy_(cnt_dev[i], non_blocking=True)
+
     t0 = time.perf_counter()
     k.stage_config_packed(host_pk_np)
     k.commit_config()
-    k.observables_device(cnt_dev[0].data_ptr())
-    cnt_host[0].copy_(cnt_dev[0], non_blocking=True)
+    counters(0)
     for s_ in range(args.e2e_steps):
         if s_ + 1 < args.e2e_steps:
             k.stage_config_packed(host_pk_np)          # H2D of the next step's input (pinned, packed)
         k.run(dt, dt, wl["scheme"])
         k.download_config_packed(host_out_np)          # D2H of the step's evolved lattice (async)
-        k.observables_device(cnt_dev[s_ + 1].data_ptr())
-        cnt_host[s_ + 1].copy_(cnt_dev[s_ + 1], non_blocking=True)   # D2H of the step's counters (async)
+        counters(s_ + 1)                                # the step's counters to the host (async)
         if s_ + 1 < args.e2e_steps:
             k.commit_config()
     k.download_wait()

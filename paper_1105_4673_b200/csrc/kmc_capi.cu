@@ -152,8 +152,10 @@ struct kmc_ctx {
     cudaEvent_t staged_ev = nullptr;         // copy + check of the staged configuration done
     cudaEvent_t consumed_ev = nullptr;       // every window that read the current spare has been enqueued before it
     bool staged = false, consumed_valid = false;
-    unsigned int* stage_err = nullptr;       // device flag of the staged check
-    unsigned int* h_stage_err = nullptr;     // pinned
+    unsigned int* stage_err = nullptr;       // device alias of h_stage_err (mapped pinned memory)
+    unsigned int* h_stage_err = nullptr;     // pinned, mapped: the staged check writes it directly (no
+                                             // D2H copy, which would queue behind a pending download
+                                             // on the device-to-host copy engine)
     // asynchronous download (kmc_download_config_packed): D2H of the planes on the copy stream; a
     // stream-ordered guard keeps the downloaded buffers unchanged until the copy has finished
     cudaEvent_t dl_ev = nullptr, dl_start_ev = nullptr;
@@ -981,7 +983,6 @@ void kmc_destroy(kmc_ctx* c) {
     if (c->consumed_ev) cudaEventDestroy(c->consumed_ev);
     if (c->dl_ev) cudaEventDestroy(c->dl_ev);
     if (c->dl_start_ev) cudaEventDestroy(c->dl_start_ev);
-    cudaFree(c->stage_err);
     if (c->h_stage_err) cudaFreeHost(c->h_stage_err);
     for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
@@ -1217,12 +1218,11 @@ kmc_status kmc_stage_config_packed(kmc_ctx* c, const uint64_t* host, int64_t nwo
     // the spare planes were current before an earlier commit: the windows enqueued before the last
     // commit may still read them
     if (c->consumed_valid) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->consumed_ev, 0));
-    CUDA_TRY(c, cudaMemsetAsync(c->stage_err, 0, 4, cs));
+    *(volatile unsigned int*)c->h_stage_err = 0u;     // the previous staged check has completed (commit)
     for (int p = 0; p < c->nplanes; ++p)
         CUDA_TRY(c, cudaMemcpyAsync(c->spare[p] + off, host + (size_t)p * owned, owned * 8, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(c, launch_check_packed(c->spare[0] + off, c->nplanes > 1 ? c->spare[1] + off : nullptr, (long long)owned,
                                     c->g.valid, c->stage_err, cs));
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_stage_err, c->stage_err, 4, cudaMemcpyDeviceToHost, cs));
     CUDA_TRY(c, cudaEventRecord(c->staged_ev, cs));
     c->staged = true;
     return KMC_OK;
@@ -1234,7 +1234,7 @@ kmc_status kmc_commit_config(kmc_ctx* c) {
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaEventSynchronize(c->staged_ev));         // normally long done: it overlapped the windows
     c->staged = false;
-    if (*c->h_stage_err)
+    if (*(volatile unsigned int*)c->h_stage_err)
         return fail(c, KMC_EINVAL, "staged packed configuration has bits outside the cells or a site both CO and O (discarded)");
     CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->staged_ev, 0));
     kmc_status sq = fused_quiesce(c);
@@ -1259,7 +1259,8 @@ static kmc_status ensure_copy_stream(kmc_ctx* c) {
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->staged_ev, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->consumed_ev, cudaEventDisableTiming));
-    if (cudaMalloc((void**)&c->stage_err, 4) != cudaSuccess || cudaMallocHost((void**)&c->h_stage_err, 4) != cudaSuccess)
+    if (cudaHostAlloc((void**)&c->h_stage_err, 4, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&c->stage_err, c->h_stage_err, 0) != cudaSuccess)
         return fail(c, KMC_ENOMEM, "staging flag allocation failed");
     return KMC_OK;
 }
@@ -1739,6 +1740,13 @@ kmc_status kmc_vgroup_observables(kmc_ctx** cs, int32_t world, kmc_obs* o) {
 kmc_status kmc_observables_device(kmc_ctx* c, uint64_t* dev_counters) {
     if (!c || !dev_counters) return fail(c, KMC_EINVAL, "NULL argument");
     CUDA_TRY(c, cudaSetDevice(c->device));
+    if (c->comm) {   // NCCL ranks all-reduce the words in place: device memory only
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, dev_counters) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+            cudaGetLastError();
+            return fail(c, KMC_EINVAL, "NCCL ranks need dev_counters in device memory");
+        }
+    }
     return enqueue_obs(c, reinterpret_cast<unsigned long long*>(dev_counters));
 }
 

@@ -1326,7 +1326,8 @@ __global__ void check_packed_kernel(const uint64_t* __restrict__ p0, const uint6
         const uint64_t b = p1 ? p1[i] : 0ull;
         bad |= ((a | b) & ~valid) != 0 || (a & b) != 0;
     }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+    // a plain store (every writer writes 1): err may be mapped pinned host memory (kmc_stage_config_packed)
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *(volatile unsigned int*)err = 1u;
 }
 
 // ---------------------------------------------------------------------------------------------
