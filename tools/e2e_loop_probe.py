@@ -16,14 +16,14 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 k = kmc.KMC(wl["ndim"], wl["dims"], wl["cell"], kind=wl["kind"], seed=1, stream=stream.cuda_stream, **wl["params"])
 lat = si.bernoulli_lattice(k.local_shape, 0.5, seed=3)
-packed = si.packed_lattice(lat, wl["ndim"], wl["cell"], 1)
+packed = si.packed_lattice(lat, wl["ndim"], wl["cell"], 2 if wl["kind"].startswith("zgb") else 1)
 hin = torch.from_numpy(packed.view(np.int64)).pin_memory().numpy().view(np.uint64).reshape(packed.shape)
 hout = torch.empty(hin.size, dtype=torch.int64).pin_memory().numpy().view(np.uint64).reshape(packed.shape)
 dt = wl["dt"]
-N = 12
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 cd = torch.zeros((N + 1, kmc.OBS_WORDS), dtype=torch.int64, device="cuda")
 ch = torch.zeros((N + 1, kmc.OBS_WORDS), dtype=torch.int64).pin_memory()
-for variant in ("mapped", "noup", "nodown", "none", "mapped", "noup", "nodown", "none"):
+for variant in ("sync", "async", "mapped", "none", "sync", "async", "mapped", "none"):
     k.stage_config_packed(hin)
     k.commit_config()
     k.run(dt, dt, wl["scheme"])

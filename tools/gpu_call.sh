@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 300 python tools/e2e_loop_probe.py ising2d_32768_strang
-nvidia-smi --query-gpu=clocks.sm,power.draw --format=csv -lms 200 > gpurun_out/clk.csv 2>&1 & P=$!
-timeout 300 python tools/e2e_loop_probe.py ising2d_32768_strang > /dev/null
-kill $P; sort gpurun_out/clk.csv | uniq -c | sort -rn | head -8
+timeout 300 python bench.py --workload diff2d_8192 --no-cpu-baseline > gpurun_out/bench_diff2d_8192.log 2> gpurun_out/bench_diff2d_8192.err; tail -1 gpurun_out/bench_diff2d_8192.log > gpurun_out/bench_diff2d_8192.json
+python -c "import json;d=json.load(open('gpurun_out/bench_diff2d_8192.json'));print(d['value'], d['e2e']['value'])"
