@@ -434,18 +434,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ne = max(1, args.e2e_steps)
-    cnt_dev = torch.zeros((ne + 1, kmc.OBS_WORDS), dtype=torch.int64, device=f"cuda:{local}")
     cnt_host = torch.zeros((ne + 1, kmc.OBS_WORDS), dtype=torch.int64).pin_memory()
 
     def counters(i):
-        # one rank: the observables kernel writes the pinned host words directly (no copy-engine
-        # transfer that would queue behind the lattice download); NCCL ranks all-reduce a device
-        # buffer, then copy it
-        if world == 1:
-            k.observables_device(cnt_host[i].data_ptr())
-        else:
-            k.observables_device(cnt_dev[i].data_ptr())
-            cnt_host[i].copy_(cnt_dev[i], non_blocking=True)
+        # the counters are written into pinned host memory by a kernel (no copy-engine transfer that
+        # would queue behind the lattice download; NCCL ranks all-reduce on the device first)
+        k.observables_device(cnt_host[i].data_ptr())
 
     t0 = time.perf_counter()
     k.stage_config_packed(host_pk_np)

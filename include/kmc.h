@@ -245,9 +245,10 @@ kmc_status kmc_observables(kmc_ctx* ctx, kmc_obs* out, uint32_t* per_cell_events
 
 /* Device-resident observables (a8 with no host round trip, e.g. once per macro-step inside a timed
  * or graph-captured loop): kmc_observables_device enqueues the counters of the current state into
- * dev_counters (KMC_OBS_WORDS uint64, caller-owned, in device memory of the context's device -- or,
- * except for NCCL ranks, in pinned host memory, which the kernel then writes directly over the bus
- * with no copy-engine transfer; KMC_EINVAL for host memory on an NCCL rank):
+ * dev_counters (KMC_OBS_WORDS uint64, caller-owned, in device memory of the context's device or in
+ * pinned host memory, which a kernel then writes directly over the bus -- no copy-engine transfer
+ * that would queue behind a pending kmc_download_config_packed; NCCL ranks all-reduce into device
+ * memory first):
  * [0..3] sites per state, [4..19] sites per state by cell colour [colour*4 + state], [20..35]
  * ordered nearest-neighbour bonds (x, x+e), e in {+x, +y}, [a*4 + b], [36] events, [37] windows,
  * [38] time (IEEE double bits), [39] 0.  Stream-ordered, asynchronous; world > 1 sums words 0..36

@@ -325,10 +325,9 @@ kmc_status exchange_forward(kmc_ctx* c) {
     NCCL_TRY(c, g_nccl.GroupEnd());
     if (c->cross) {   // snapshot the ghost rows so the sub-step's writes into them can be sent back
         for (int p = 0; p < c->nplanes; ++p) {
-            CUDA_TRY(c, cudaMemcpyAsync(c->ghost_snap + (size_t)(2 * p) * rowlen, c->planes[p], rowlen * 8,
-                                        cudaMemcpyDeviceToDevice, c->stream));
-            CUDA_TRY(c, cudaMemcpyAsync(c->ghost_snap + (size_t)(2 * p + 1) * rowlen, c->planes[p] + (size_t)(My + 1) * rowlen,
-                                        rowlen * 8, cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_TRY(c, launch_copy_u64(c->ghost_snap + (size_t)(2 * p) * rowlen, c->planes[p], (long long)rowlen, c->stream));
+            CUDA_TRY(c, launch_copy_u64(c->ghost_snap + (size_t)(2 * p + 1) * rowlen, c->planes[p] + (size_t)(My + 1) * rowlen,
+                                        (long long)rowlen, c->stream));
         }
     }
     return KMC_OK;
@@ -1024,7 +1023,7 @@ static kmc_status swap_in_spare(kmc_ctx* c) {
     if (sq != KMC_OK) return sq;
     for (int p = 0; p < c->nplanes; ++p) {
         if (in_place)
-            CUDA_TRY(c, cudaMemcpyAsync(c->planes[p], c->spare[p], (size_t)c->plane_words * 8, cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_TRY(c, launch_copy_u64(c->planes[p], c->spare[p], c->plane_words, c->stream));
         else
             std::swap(c->spare[p], c->planes[p]);
     }
@@ -1243,8 +1242,8 @@ kmc_status kmc_commit_config(kmc_ctx* c) {
     if (c->g.ghost) {   // ghost rows are refreshed by the next exchange; keep them defined (stream-ordered)
         const size_t row = (size_t)c->g.R * c->g.Mx, last = (size_t)(c->g.My_local + 1) * row;
         for (int p = 0; p < c->nplanes; ++p) {
-            CUDA_TRY(c, cudaMemcpyAsync(c->spare[p], c->planes[p], row * 8, cudaMemcpyDeviceToDevice, c->stream));
-            CUDA_TRY(c, cudaMemcpyAsync(c->spare[p] + last, c->planes[p] + last, row * 8, cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_TRY(c, launch_copy_u64(c->spare[p], c->planes[p], (long long)row, c->stream));
+            CUDA_TRY(c, launch_copy_u64(c->spare[p] + last, c->planes[p] + last, (long long)row, c->stream));
         }
     }
     kmc_status st = swap_in_spare(c);
@@ -1681,7 +1680,7 @@ kmc_status kmc_observables(kmc_ctx* c, kmc_obs* o, uint32_t* per_cell) {
     const bool mapped = !c->comm;
     kmc_status st = enqueue_obs(c, mapped ? c->d_hobs : c->obs_buf);
     if (st != KMC_OK) return st;
-    if (!mapped) CUDA_TRY(c, cudaMemcpyAsync(c->h_obs, c->obs_buf, KMC_OBS_WORDS * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (!mapped) CUDA_TRY(c, launch_copy_words(c->d_hobs, c->obs_buf, KMC_OBS_WORDS, c->stream));   // no copy engine
     if (c->fused_ipc) CUDA_TRY(c, cudaMemcpyAsync(c->h_flag, c->flags + 2, 8, cudaMemcpyDeviceToHost, c->stream));
     std::vector<uint32_t> wl;
     const long long owned = (long long)c->g.My_local * c->g.R * c->g.Mx;
@@ -1740,11 +1739,18 @@ kmc_status kmc_vgroup_observables(kmc_ctx** cs, int32_t world, kmc_obs* o) {
 kmc_status kmc_observables_device(kmc_ctx* c, uint64_t* dev_counters) {
     if (!c || !dev_counters) return fail(c, KMC_EINVAL, "NULL argument");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    if (c->comm) {   // NCCL ranks all-reduce the words in place: device memory only
+    if (c->comm) {   // NCCL ranks all-reduce a device buffer; host destinations get it by a copy kernel
         cudaPointerAttributes at{};
-        if (cudaPointerGetAttributes(&at, dev_counters) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+        if (cudaPointerGetAttributes(&at, dev_counters) != cudaSuccess) {
             cudaGetLastError();
-            return fail(c, KMC_EINVAL, "NCCL ranks need dev_counters in device memory");
+            return fail(c, KMC_EINVAL, "dev_counters is neither device nor pinned host memory");
+        }
+        if (at.type != cudaMemoryTypeDevice) {
+            kmc_status st = enqueue_obs(c, c->obs_buf);
+            if (st != KMC_OK) return st;
+            CUDA_TRY(c, launch_copy_words(reinterpret_cast<unsigned long long*>(dev_counters), c->obs_buf,
+                                          KMC_OBS_WORDS, c->stream));
+            return KMC_OK;
         }
     }
     return enqueue_obs(c, reinterpret_cast<unsigned long long*>(dev_counters));

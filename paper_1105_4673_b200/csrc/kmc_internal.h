@@ -139,5 +139,7 @@ cudaError_t launch_wait_flags(unsigned long long* flags, unsigned long long epoc
 cudaError_t launch_signal_flags(unsigned long long* up_flags, unsigned long long* dn_flags, unsigned long long v,
                                 cudaStream_t s);
 cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* a, const uint64_t* b, long long n, cudaStream_t s);
+cudaError_t launch_copy_words(unsigned long long* dst, const unsigned long long* src, int n, cudaStream_t s);
+cudaError_t launch_copy_u64(uint64_t* dst, const uint64_t* src, long long n, cudaStream_t s);
 
 }  // namespace kmc

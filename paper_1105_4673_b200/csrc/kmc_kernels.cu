@@ -1409,4 +1409,32 @@ cudaError_t launch_xor_rows(uint64_t* dst, const uint64_t* src, const uint64_t* 
     return cudaGetLastError();
 }
 
+// a few words device -> (mapped pinned host) memory by a kernel: no copy-engine transfer, so it does
+// not queue behind a large download on the device-to-host engine
+__global__ void copy_words_kernel(unsigned long long* dst, const unsigned long long* src, int n) {
+    const int i = threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
+// device-to-device copy of n u64 words by a kernel: the per-step row / plane copies stay off the copy
+// engines, where they would queue behind an asynchronous lattice download
+__global__ void copy_u64_kernel(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t launch_copy_u64(uint64_t* dst, const uint64_t* src, long long n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    long long nb = (n + 255) / 256;
+    if (nb > 148 * 8) nb = 148 * 8;
+    copy_u64_kernel<<<(unsigned)nb, 256, 0, s>>>(dst, src, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy_words(unsigned long long* dst, const unsigned long long* src, int n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    copy_words_kernel<<<1, 64, 0, s>>>(dst, src, n);
+    return cudaGetLastError();
+}
+
 }  // namespace kmc
