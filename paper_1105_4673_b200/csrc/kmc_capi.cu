@@ -443,11 +443,13 @@ static SubstepArgs window_args(const kmc_ctx* c, int colour, double D, uint64_t 
     }
     // refill batching of the window kernel (performance only; results are bit-identical): a warp
     // refills its finished lanes once refill_min of them are parked.  Best thresholds measured on
-    // B200 (tools/sweep_refill.sh) depend on the expected events per cell-window mu ~ D x
-    // rate_per_cell: mu >= 16 (Ising dt = 1, diffusion): spin flip 3, diffusion 4; mu < 16
-    // (Ising dt = 0.01, ZGB dt = 0.1): spin flip 10, ZGB 16 (+8 % over 8).  Env KMC_REFILL overrides.
+    // B200 (KMC_REFILL sweeps) fall with the events per cell-window mu: mu >= 16 (D x rate_per_cell,
+    // Ising dt = 1, diffusion dt = 1): spin flip 3, diffusion 4; below (dt = 0.01, ZGB at dt = 0.1):
+    // spin flip 10 (flat from 2 to 12 at mu ~ 0.8), diffusion 10, ZGB 14 (mu ~ 2.3; 2.105e10 vs 1.94e10
+    // at 8), ZGB + CO hops 10 (mu ~ 4.3; +4 % over 16), ZGB + O hops 8 (mu ~ 6.5; +10 % over 16).
+    // Env KMC_REFILL overrides.
     static const int refill_env = [] { const char* e = getenv("KMC_REFILL"); return e ? atoi(e) : 0; }();
-    static const int refill_hi[5] = {3, 4, 6, 6, 6}, refill_lo[5] = {10, 10, 16, 16, 16};   // by model kind
+    static const int refill_hi[5] = {3, 4, 6, 6, 6}, refill_lo[5] = {10, 10, 14, 10, 8};   // by model kind
     a.refill_min = refill_env >= 1 && refill_env <= 32 ? refill_env
                  : (D * c->rate_per_cell >= 16.0 ? refill_hi[c->kind] : refill_lo[c->kind]);
     const uint64_t w = c->window + ahead;

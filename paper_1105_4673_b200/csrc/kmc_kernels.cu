@@ -17,7 +17,10 @@
 //   give 32x the issue efficiency of a warp-cooperative scan.  The event steps are in
 //   kmc_device.cuh: event_step (generic, every model; also used by the tile kernel of
 //   kmc_tile.cu), event_step_hop (diffusion, n-major hop blocks, R31; KIND 4) and
-//   event_step_zgb_grouped (ZGB with one rate per direction group; KINDs 5, 6).
+//   event_step_zgb_grouped (ZGB with one rate per direction group; KINDs 5, 6, 8).  Every 2D
+//   variant is also built for 8 x 8 cells with the shape as a compile-time constant (SQ = 8).
+// substep_group_kernel: the same window with g lanes per cell for windows with few active cells
+//   (small lattices): the g lanes draw g consecutive events in parallel, then run them in order.
 // observables_kernel (a8): integer counts, order-free, one launch per observation.
 // correlation_kernel, series_*_kernel (f1): pair counts; the coverage process and its statistics.
 // strip / cdf kernels (f4), init_random_kernel (R32), pack / unpack (uint8 site-major <->
