@@ -29,6 +29,21 @@ def test_reference_arm_json_line(workload):
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
 
 
+def test_gpus_n_relaunches_one_process_per_rank():
+    """`bench.py --gpus 2` without WORLD_SIZE re-launches itself under torchrun (one process per
+    rank, 127.0.0.1 rendezvous); with the reference arm that runs on CPU: rank 0 alone prints one
+    line with n_gpus = 2 and the other rank exits 0."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--workload", "ising1d_65536x64", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["workload"] == "ising1d_65536x64"
+
+
 def test_config_and_l2_policy():
     import bench
     import synth_inputs as si
