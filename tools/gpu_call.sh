@@ -1,6 +1,10 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "kernel_modes or full_size or sampled or maximum" > gpurun_out/tp.log 2>&1; echo tp rc=$?; tail -3 gpurun_out/tp.log
-for r in 1 2; do for T in 0 1; do
-for w in "ising2d_32768 --dt 0.01" "ising2d_32768 --dt 0.05" "ising2d_32768 --dt 0.003"; do
-  KMC_TWOPASS=$T timeout 300 python bench.py --no-cpu-baseline --workload $w --steps 20 --warmup 3 --e2e-steps 0 2>/dev/null | tail -1 | python -c "import json,sys;d=json.load(sys.stdin);print('twopass=$T', d['config']['workload'], d['config']['dt'], '%.4g'%d['value'], 'su/s %.4g'%d['site_updates_per_s'])"
-done; done; done
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/final_smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/final_smoke.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/final_tests.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/final_tests.log
+timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; echo bench rc=$?
+timeout 600 python bench.py --impl reference > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err; echo ref rc=$?
+python -c "
+import json
+d=json.loads(open('gpurun_out/final_bench.json').read().strip().splitlines()[-1])
+print('value %.4g e2e %.4g frac %.3f alg %.3f clocks %s cpu %.3g launches %d' % (d['value'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['frac_algorithmic'], d['clocks'], d['cpu_baseline']['value'], d['gpu_launches']))
+r=json.loads(open('gpurun_out/final_ref.json').read().strip().splitlines()[-1]); print('ref %.4g' % r['value'])"
