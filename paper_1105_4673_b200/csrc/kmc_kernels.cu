@@ -27,6 +27,10 @@
 // bit-packed cell-major), exchange helpers (flags, XOR rows) for the multi-GPU slabs.
 #include "kmc_device.cuh"
 
+#ifndef GROUP_SPEC
+#define GROUP_SPEC 1   // lane-group kernel, spin flip: speculative event application (see group_window)
+#endif
+
 #include <cassert>
 #include <cstdint>
 #include <cstdlib>
@@ -374,6 +378,52 @@ __device__ __forceinline__ unsigned long long group_window(const SubstepArgs& a,
         // is events k + G .. k + 2G - 1
         const uint4 xn = philox_event(a, cl.k + G + sub, cl.gid32);
         const double En = exp_variate(a, xn, s_logt);
+        if constexpr (KIND == 0 && GROUP_SPEC) {
+            // spin flip: the G events applied speculatively (each as if accepted), then the state
+            // after the last accepted one kept: P before event j is snapshotted, the first rejected
+            // event ends the window (R5) and the later ones are discarded
+            uint64_t snap[G];
+            double tsnap[G + 1];
+            bool accj[G];
+            tsnap[0] = cl.tclock;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                const int src = (int)(base | (uint32_t)j);
+                uint4 xj;
+                xj.x = 0u;
+                xj.y = 0u;
+                xj.z = __shfl_sync(FULL, xd.z, src);
+                xj.w = __shfl_sync(FULL, xd.w, src);
+                const double Ej = __hiloint2double(__shfl_sync(FULL, __double2hiint(Ed), src),
+                                                   __shfl_sync(FULL, __double2loint(Ed), src));
+                snap[j] = cl.P[0];
+                event_step<KIND, NDIM, MH, true, SQ, true>(a, cl.P, cl.h, cl.k, cl.tclock, cl.gid32, have, s_logt,
+                                                           s_sel8, xj, Ej, &accj[j]);
+                tsnap[j + 1] = cl.tclock;
+            }
+            int nacc = 0;                                    // accepted events before the first rejection
+            bool run = true;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                run = run && accj[j];
+                nacc += run ? 1 : 0;
+            }
+            uint64_t Pk = cl.P[0];
+            double tk = tsnap[G];
+#pragma unroll
+            for (int j = G - 1; j >= 0; --j) {
+                Pk = nacc == j ? snap[j] : Pk;
+                tk = nacc == j ? tsnap[j] : tk;
+            }
+            cl.P[0] = Pk;
+            cl.tclock = tk;
+            cl.k += (uint32_t)nacc;
+            have = have && nacc == G;
+            if (!__any_sync(FULL, have)) break;
+            xd = xn;
+            Ed = En;
+            continue;
+        }
 #pragma unroll
         for (int j = 0; j < G; ++j) {
             const int src = (int)(base | (uint32_t)j);
