@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/final_tests.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/final_tests.log
-for w in ising2d_1024 ising1d_65536 noninteracting1d_1024x1000; do
-  timeout 300 python bench.py --workload $w --no-cpu-baseline > gpurun_out/bench_$w.log 2> gpurun_out/bench_$w.err; tail -1 gpurun_out/bench_$w.log > gpurun_out/bench_$w.json
-  python -c "import json;d=json.load(open('gpurun_out/bench_$w.json'));print('$w', d['value'], d['e2e']['value'])"
-done
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/bs.log 2>&1; echo tests rc=$?; tail -1 gpurun_out/bs.log
+for r in 1 2; do for L in abtmp/libkmc_base.so paper_1105_4673_b200/libkmc_b200.so; do
+for w in "ising2d_32768" "ising2d_32768_strang" "ising2d_32768 --dt 0.01" "diff2d_8192" "ising2d_1024"; do
+  KMC_B200_LIB=$L timeout 300 python bench.py --no-cpu-baseline --workload $w --steps 20 --warmup 3 --e2e-steps 0 2>/dev/null | tail -1 | python -c "import json,sys;d=json.load(sys.stdin);print('$L', d['config']['workload'], d['config']['dt'], '%.4g'%d['value'])"
+done; done; done
