@@ -64,6 +64,8 @@ CASES = {
     "2d_ising_random": (2, (64, 64), (8, 8), "adsdes", dict(ca=1, cd=1, beta=2.2, K=1.0, h=-2.0), 0, 2, 0.9, "random", 1.0, 2),
     "2d_ising_rect_cell": (2, (64, 128), (2, 16), "adsdes", dict(ca=1, cd=1, beta=1.0, K=1.0, h=-2.0), 0, 1, 0.5, "strang", 0.5, 2),
     "2d_ising_1x1_cell": (2, (16, 16), (1, 1), "adsdes", dict(ca=1, cd=1, beta=1.0, K=1.0, h=-2.0), 0, 3, 0.5, "lie", 0.7, 3),
+    # quiescent cells: no adsorption (c_a = 0), so every cell whose sites are all vacant has lambda = 0
+    "2d_ising_quiescent": (2, (64, 64), (8, 8), "adsdes", dict(ca=0.0, cd=1.0, beta=1.0, K=1.0, h=-2.0), 0, 2, 0.02, "strang", 1.0, 3),
     "2d_ising_ragged": (2, (24, 40), (4, 4), "adsdes", dict(ca=0.7, cd=1.3, beta=1.2, K=0.8, h=-1.0), 0, 5, 0.4, "strang", 1.0, 2),
     "2d_diffusion_4col": (2, (64, 64), (8, 8), "adsdes_diff", dict(ca=1, cd=1, beta=1.5, K=1.0, h=-2.0, c_hop=1.0), 0, 1, 0.5, "strang", 0.5, 2),
     "2d_diffusion_q2": (2, (32, 32), (2, 2), "adsdes_diff", dict(ca=0.3, cd=0.3, beta=1.0, K=1.0, h=-2.0, c_hop=2.0), 0, 2, 0.5, "lie", 0.5, 2),
