@@ -924,11 +924,16 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
     ok = ok && alloc((void**)&c->obs_buf, KMC_OBS_WORDS * 8);
     ok = ok && alloc((void**)&c->logtab, kLogTab * sizeof(double2));
     if (ok) {   // log_spec tables, host libm; uploaded once
-        double2 tab[kLogTab];
-        for (int j = 0; j < kLogTab; ++j) {
-            tab[j].x = 128.0 / (double)(j + 91);
-            tab[j].y = -std::log(tab[j].x);
+        double2 bucket[kLogBuckets], tab[kLogTab];
+        for (int j = 0; j < kLogBuckets; ++j) {
+            bucket[j].x = 128.0 / (double)(j + 91);
+            bucket[j].y = -std::log(bucket[j].x);
         }
+        // entry i -> bucket j = round(128 m) - 91 of the mantissas with high bits t:
+        // not halved (t <= 0x6A, i = t): j = 128 + ((t + 1) >> 1) - 91; halved (i = t + 1, t >= 0x6A):
+        // j = 64 + ((t + 2) >> 2) - 91.  Both stay in [0, 90].
+        for (int i = 0; i < kLogTab; ++i)
+            tab[i] = bucket[i <= 0x6A ? 37 + ((i + 1) >> 1) : ((i + 1) >> 2) - 27];
         ok = cudaMemcpy(c->logtab, tab, sizeof tab, cudaMemcpyHostToDevice) == cudaSuccess;
     }
     ok = ok && alloc((void**)&c->obs_acc, (kObsCounters + 1) * 8) &&

@@ -16,7 +16,8 @@
 namespace kmc {
 
 constexpr int kMaxClass = 32;
-constexpr int kLogTab = 91;          // buckets of the table-driven log
+constexpr int kLogBuckets = 91;      // buckets j of the table-driven log
+constexpr int kLogTab = 257;         // lookup entries: bucket of (mantissa bits 51..44 t, halved?) at t + halved
 
 // Slot types, used by the host rate table.
 enum SlotType { T_ADS = 0, T_DES = 1, T_HOP = 2, T_COADS = 3, T_O2ADS = 4, T_RCO = 5, T_RO = 6, T_COHOP = 7, T_OHOP = 8 };
@@ -58,9 +59,10 @@ struct SubstepArgs {
     uint64_t rate[kMaxClass];        // u64 fixed-point class rates (R18)
     uint64_t hopz[4];                // ADSDES_DIFF: (z - n) x the hop rate of block n (uniform blocks, R31)
     int hop_fast;                    // every hop block (ADSDES_DIFF) / direction group (ZGB) has one rate
-    const double2* logtab;           // log_spec table {c_j, L_j}, kLogTab entries in device
-                                     // memory: c_j = 128/(j+91), L_j = -log(c_j) (host libm); kept out of
-                                     // the parameters so a launch copies ~0.8 KB instead of ~2.3 KB
+    const double2* logtab;           // log_spec lookup {c_j, L_j}, kLogTab entries in device
+                                     // memory: c_j = 128/(j+91), L_j = -log(c_j) (host libm), entry i holding
+                                     // the bucket j of the mantissas with t = mant >> 44 = i (not halved,
+                                     // i <= 0x6A) or t = i - 1 (halved, i >= 0x6B); kept out of the parameters
     double lcoef[6];                 //   {1/7, -1/6, 1/5, 1/3, ln2_hi, ln2_lo} (exact hex literals)
     // fused halo exchange (SURVEY §8(e) "later option"): the window kernel mirrors every write to a
     // boundary-row or ghost-row word into the neighbour ranks' planes (peer pointers: other slabs on
