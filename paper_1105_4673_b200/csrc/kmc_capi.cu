@@ -932,8 +932,12 @@ static kmc_status create_ctx(const kmc_geometry* geom, const kmc_model* model, c
         // entry i -> bucket j = round(128 m) - 91 of the mantissas with high bits t:
         // not halved (t <= 0x6A, i = t): j = 128 + ((t + 1) >> 1) - 91; halved (i = t + 1, t >= 0x6A):
         // j = 64 + ((t + 2) >> 2) - 91.  Both stay in [0, 90].
-        for (int i = 0; i < kLogTab; ++i)
+        // Halved entries hold c_j / 2 (exact): log_spec multiplies the unhalved mantissa by them,
+        // (2m) (c_j / 2) = m c_j exactly, so r = fma(., ., -1) rounds the same real number.
+        for (int i = 0; i < kLogTab; ++i) {
             tab[i] = bucket[i <= 0x6A ? 37 + ((i + 1) >> 1) : ((i + 1) >> 2) - 27];
+            if (i > 0x6A) tab[i].x *= 0.5;
+        }
         ok = cudaMemcpy(c->logtab, tab, sizeof tab, cudaMemcpyHostToDevice) == cudaSuccess;
     }
     ok = ok && alloc((void**)&c->obs_acc, (kObsCounters + 1) * 8) &&
