@@ -13,6 +13,7 @@ Prints ONE JSON line on rank 0.
 """
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -279,7 +280,8 @@ def main():
     ap.add_argument("--dt", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None,
-                    help="steps of the end-to-end measurement (default: --steps, like the device-timed loop)")
+                    help="steps of the end-to-end measurement (default: --steps, raised to span >= 0.25 s of "
+                         "device time so host jitter cannot dominate short steps)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: one workload-sized slab per GPU (default); strong: the workload split over the GPUs")
     ap.add_argument("--fused-exchange", action="store_true",
@@ -288,7 +290,8 @@ def main():
                     help="N = 1, 2D: run the lattice as a one-rank ring through the multi-GPU data plane "
                          "(NCCL send/recv to itself, or the fused exchange) to measure its cost on one GPU")
     args = ap.parse_args()
-    if args.e2e_steps is None:
+    args.e2e_auto = args.e2e_steps is None
+    if args.e2e_auto:
         args.e2e_steps = args.steps
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch this command under torchrun (the driver's own N > 1 launch
@@ -423,6 +426,10 @@ def main():
     # runs on the next committed configuration).  Every copy is complete inside the timed region.
     # The uploaded input is the lattice the timed steps reached (downloaded once, untimed), so every
     # e2e step runs the steady-state workload.
+    if args.e2e_auto and args.e2e_steps > 0:
+        # short steps (launch-bound 1D lattices, small dt): enough steps for >= 0.25 s of device time
+        # (ms is the max over ranks, so every rank takes the same count)
+        args.e2e_steps = max(args.e2e_steps, min(20000, math.ceil(250.0 / max(ms / args.steps, 1e-3))))
     host_pk_np[...] = k.get_config_packed()
     k.stage_config_packed(host_pk_np)                   # untimed e2e warm-up (first calls allocate
     k.commit_config()                                   # the spare planes and the copy stream)

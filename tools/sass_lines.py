@@ -10,7 +10,7 @@ import tempfile
 want = sys.argv[1] if len(sys.argv) > 1 else "_ZN3kmc14substep_kernelILi0ELi2ELi256ELi4ELb0ELb0ELb0EEEvNS_11SubstepArgsEjj"
 cubin_name = sys.argv[2] if len(sys.argv) > 2 else "kmc_kernels.sm_100a.cubin"
 d = tempfile.mkdtemp()
-subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath("paper_1105_4673_b200/libkmc_b200.so")], cwd=d,
+subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(os.environ.get("KMC_B200_LIB", "paper_1105_4673_b200/libkmc_b200.so"))], cwd=d,
                capture_output=True)
 txt = subprocess.run(["nvdisasm", "-g", os.path.join(d, cubin_name)], capture_output=True, text=True).stdout
 line = None
