@@ -1,11 +1,12 @@
 """Print the instruction count of the main event loop (largest backward branch span) of a kernel
 in libkmc_b200.so, with an opcode histogram: a cheap pre-GPU check of per-event cost."""
 import collections
+import os
 import re
 import subprocess
 import sys
 
-lib = "paper_1105_4673_b200/libkmc_b200.so"
+lib = os.environ.get("KMC_B200_LIB", "paper_1105_4673_b200/libkmc_b200.so")
 want = sys.argv[1] if len(sys.argv) > 1 else "ILi0ELi2ELi256ELi4ELb0ELb0ELb0E"
 out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s*Function : ", out)
