@@ -35,13 +35,7 @@
 #include <cstdint>
 #include <cstdlib>
 
-// Debug builds (KMC_NVCC_FLAGS=-DKMC_DEBUG_BOUNDS) check every computed word index against its
-// buffer with a device assert (the bounds check used instead of compute-sanitizer).
-#ifdef KMC_DEBUG_BOUNDS
-#define KMC_BOUNDS(cond) assert(cond)
-#else
-#define KMC_BOUNDS(cond) ((void)0)
-#endif
+// KMC_BOUNDS (debug builds, KMC_NVCC_FLAGS=-DKMC_DEBUG_BOUNDS): kmc_device.cuh
 
 namespace kmc {
 
@@ -158,7 +152,7 @@ __device__ __forceinline__ void mirror_word(const SubstepArgs& a, int p, uint32_
 template <int KIND, int NDIM, bool MH, bool NEST, bool PEER, int SQ = 0>
 struct Cell {
     static constexpr int NP = Model<KIND, NDIM>::NP;
-    uint64_t P[NP], h[NP][4];
+    uint64_t P[NP] = {}, h[NP][4] = {};   // zero until the first load: idle lanes step on a consistent empty cell
     uint32_t gid32 = 0, k = 0, iCcur = 0;
     uint32_t wrap = 0;   // hop / pair models: which neighbour indices wrap (W, E, N, S), for the store
     uint32_t srow = 0;   // PEER: storage row of the current cell

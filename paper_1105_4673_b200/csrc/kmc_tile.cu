@@ -70,7 +70,7 @@ tile_kernel_adsdes2d(const SubstepArgs a, const int tiles_x) {
     int lr = 0, lc = 0;
     uint32_t gid32 = 0, k = 0;
     double tclock = 0.0;
-    uint64_t P[1], hb[1][4];
+    uint64_t P[1] = {}, hb[1][4] = {};
     unsigned long long evsum = 0;
     auto load = [&]() {
         cell_of(t, lr, lc);
